@@ -1,0 +1,137 @@
+/*
+ * aifmm.h — C-ABI of libaifmm.so, the B200 (sm_100a) AIFMM hot path.
+ *
+ * The operation (PAPER.md, cited as P:<line>):
+ *   Solve A x = b for dense N-body matrices A_ij = K(x_i, x_j) (problem statement
+ *   P:105-111; targets = sources) with the Algebraic Inverse Fast Multipole
+ *   Method: a 2^d tree (§2.1), strong admissibility / interaction lists
+ *   (§2.2), NNCA far-field operators (§2.3 Eq. NCA), the extended
+ *   sparse system (§3.1), level-by-level elimination with deferred (Alg. 3,
+ *   P:1107-1164) compression and redirection of far fill-ins (§3.2.1-3.2.3),
+ *   and back substitution (Alg. 4).  The factorization is independent of b
+ *   (Remark P:1186-1188): build + factor once, solve many times.
+ *
+ * Conventions
+ *   - One implicit context per process (one process per GPU).  Calls are serialised by
+ *     the caller; there is no internal locking.
+ *   - "device" pointers are CUDA device pointers on the current device; "host" pointers
+ *     are ordinary (pageable or pinned) host memory.
+ *   - Matrices are column-major.  Points are N x d row-major (point i at points[i*d]).
+ *   - Every function returns 0 on success or a negative AIFMM_E* code; the message is
+ *     available from aifmm_last_error().  No C++ exception crosses this boundary.
+ *   - Floating point is IEEE binary64 throughout (the paper's double / BASELINE FP64).
+ */
+#ifndef AIFMM_H
+#define AIFMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes. */
+#define AIFMM_OK                   0
+#define AIFMM_EINVALID_ARG        -1  /* n < 1, d not 2|3, leaf_size < 1, tol not in (0,1), nrhs < 1, NULL */
+#define AIFMM_ENONFINITE          -2  /* NaN/Inf in points or B                                         */
+#define AIFMM_ECOINCIDENT         -3  /* two coincident points with a singular kernel (log r, 1/r)      */
+#define AIFMM_ESINGULAR_SKELETON  -4  /* NNCA skeleton block A(fp, sk) singular                          */
+#define AIFMM_ESINGULAR_PIVOT     -5  /* a box pivot [[K, U],[V^*, 0]] or the top system is singular     */
+#define AIFMM_ESTATE              -6  /* factor before build, solve before factor                        */
+#define AIFMM_ECUDA               -7  /* CUDA runtime error                                              */
+#define AIFMM_ENCCL               -8  /* NCCL error (multi-GPU)                                          */
+#define AIFMM_EOOM                -9  /* device memory exhausted                                         */
+
+/* Kernel ids (BASELINE.json configs; kparams = {diag, ell}):
+ *   0  log r         A_ii = diag            (configs 1, 2)
+ *   1  exp(-r/ell)   A_ii = diag (1+nugget) (config 3, Matern-1/2)
+ *   2  1/r           A_ii = diag            (configs 4, 5; paper Exp. 3 with diag sqrt(1000N)) */
+
+/* aifmm_build — tree, lists, colouring and NNCA operators (the paper's assembly, T_Aa).
+ *   points    device, n x d row-major float64, user order.  Copied; the caller may free it
+ *             after the call returns.
+ *   n, d      number of points (>= 1), dimension (2 or 3).
+ *   kernel_id 0|1|2 (above).  kparams: host, 2 doubles {diag, ell}.
+ *   leaf_size n_max: leaves hold no more than n_max points, depth L >= 2.
+ *   tol       eps_A in (0,1): NNCA (ACA at tol/100, reading R18) and RRQR truncation tol.
+ * Discards any previous build/factorization.  Errors: EINVALID_ARG, ENONFINITE,
+ * ECOINCIDENT, ESINGULAR_SKELETON, ECUDA, EOOM. */
+int aifmm_build(const double* points, int64_t n, int d, int kernel_id,
+                const double* kparams, int leaf_size, double tol);
+
+/* aifmm_set_compression_tol — optional, before aifmm_factor: the fill-in truncation
+ * tolerance tol_c (default = tol).  tol_c = 0 keeps every fill-in direction (exact
+ * redirection; used by the tests to separate NNCA error from compression error). */
+int aifmm_set_compression_tol(double tol_c);
+
+/* aifmm_factor — elimination with colour-batched Algorithm 3 (T_Af).
+ * Needs a successful build.  Errors: ESTATE, ESINGULAR_PIVOT, ECUDA, EOOM. */
+int aifmm_factor(void);
+
+/* aifmm_solve — Algorithm 4 for nrhs right-hand sides (T_As).
+ *   B     device, n x nrhs column-major (ld = n), user order; overwritten by X.
+ *   nrhs  >= 1.
+ * Errors: ESTATE, EINVALID_ARG, ENONFINITE, ECUDA, EOOM. */
+int aifmm_solve(double* B, int nrhs);
+
+/* aifmm_solve_host — the same through host buffers: B (host, n x nrhs column-major) is
+ * copied to the device, solved and copied back (end-to-end path used by bench.py e2e). */
+int aifmm_solve_host(double* B, int nrhs);
+
+/* aifmm_free — release every device buffer of the context. */
+void aifmm_free(void);
+
+/* aifmm_last_error — message of the last failing call ("" if none). Owned by the library. */
+const char* aifmm_last_error(void);
+
+/* aifmm_set_stream — optional: run on the given cudaStream_t (default: a library stream). */
+int aifmm_set_stream(void* stream);
+
+/* Introspection for parity tests (integer outputs are bit-exact with the oracle). */
+/* aifmm_get_tree — perm: host int64[n] (perm[j] = user index of the j-th point in tree
+ * order); L: host int*; either may be NULL. */
+int aifmm_get_tree(int64_t* perm, int* L);
+/* aifmm_get_level_offsets — host int64[2^(d*level)+1]: point offsets of every box. */
+int aifmm_get_level_offsets(int level, int64_t* off);
+/* aifmm_get_lists — CSR over the 2^(d*level) boxes (empty boxes have empty lists):
+ * n_ptr/il_ptr host int32[2^(d*level)+1]; n_idx/il_idx host int32 of size n_ptr[last] /
+ * il_ptr[last] (query sizes first by passing NULL idx arrays).  Lists are Morton-sorted. */
+int aifmm_get_lists(int level, int32_t* n_ptr, int32_t* n_idx, int32_t* il_ptr, int32_t* il_idx);
+/* aifmm_get_colours — host int32[2^(d*level)]: colour of each box (-1 for empty boxes). */
+int aifmm_get_colours(int level, int32_t* colour);
+/* aifmm_get_ranks — host int32[2^(d*level)]: NNCA rank (which = 0) or final rank after
+ * factorization (which = 1) of every box (0 for empty boxes). */
+int aifmm_get_ranks(int level, int which, int32_t* ranks);
+
+/* aifmm_stats — host double[AIFMM_NSTATS], see the AIFMM_STAT_* indices. */
+#define AIFMM_NSTATS 16
+#define AIFMM_STAT_BUILD_MS        0
+#define AIFMM_STAT_FACTOR_MS       1
+#define AIFMM_STAT_SOLVE_MS        2
+#define AIFMM_STAT_LEVELS          3
+#define AIFMM_STAT_TOP_SIZE        4
+#define AIFMM_STAT_FACTOR_FLOPS    5   /* algorithmic FLOPs of the factorization (model) */
+#define AIFMM_STAT_SCHUR_FLOPS     6   /* FLOPs of the Schur-update GEMM launches                        */
+#define AIFMM_STAT_SCHUR_MS        7   /* device time of the Schur-update GEMM launches (CUDA events)    */
+#define AIFMM_STAT_LAUNCHES        8   /* kernels launched by the library since the last reset           */
+#define AIFMM_STAT_COMPRESSIONS    9
+#define AIFMM_STAT_MAX_RANK       10
+#define AIFMM_STAT_DEVICE_BYTES   11
+#define AIFMM_STAT_SCHUR_BYTES    12   /* algorithmic bytes of the Schur-update launches                */
+#define AIFMM_STAT_SCHUR_LAUNCHES 13
+#define AIFMM_STAT_SOLVE_BYTES    14
+#define AIFMM_STAT_HOST_SYNCS     15
+int aifmm_stats(double* out);
+/* aifmm_reset_counters — zero the launch / FLOP / time counters. */
+int aifmm_reset_counters(void);
+/* aifmm_set_timing — 1: record CUDA events around the Schur launches (for bench roofline). */
+int aifmm_set_timing(int on);
+
+/* Test hook: in-place inverse of one n x n column-major device matrix with the library's
+ * batched Gauss-Jordan (R16; the kernel behind pivot inverses and the top solve). */
+int aifmm_debug_inverse(double* A, int n, int lda);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AIFMM_H */

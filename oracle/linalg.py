@@ -8,6 +8,8 @@ then broken identically on CPU and GPU, although the two round differently.
 R8 pivoted-QR truncation (the paper's RRQR, "relative residual ...
 O(eps_A)"): column-pivoted Gram-Schmidt with re-orthogonalisation; after t
 steps the residual is W_t = (I - Q_t Q_t^T) W; stop when ||W_t||_F <= tau.
+A pivot column whose re-orthogonalised norm keeps collapsing (it lies in the span
+of the basis to working precision) is discarded rather than normalised.
 """
 from __future__ import annotations
 
@@ -54,10 +56,19 @@ def pivoted_qr_extend(W: np.ndarray, basis: np.ndarray, tau: float, tmin: int, t
         if j is None:
             break
         w = W[:, j].copy()
-        # re-orthogonalise twice against everything taken so far (R8)
+        # R8 re-orthogonalisation against everything taken so far: two passes, a third
+        # if the second cancelled more than half; a column still collapsing after the
+        # third pass lies in span(B) numerically and is discarded
         w = w - B @ (B.T @ w)
+        n1 = np.linalg.norm(w)
         w = w - B @ (B.T @ w)
         nw = np.linalg.norm(w)
+        if not nw > 0.5 * n1:
+            n2 = nw
+            w = w - B @ (B.T @ w)
+            nw = np.linalg.norm(w)
+            if not nw > 0.5 * n2:
+                nw = 0.0
         if not nw > 0.0:
             W[:, j] = 0.0
             continue

@@ -1,0 +1,184 @@
+"""Thin Python binding of libaifmm.so (include/aifmm.h): argument marshalling only.
+
+Every step of build / factor / solve runs in the library's sm_100a kernels; torch is used
+for device memory only.  There is no CPU fallback: importing this module without the
+built library, or calling it without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libaifmm.so")
+
+ERRORS = {
+    -1: "EINVALID_ARG", -2: "ENONFINITE", -3: "ECOINCIDENT", -4: "ESINGULAR_SKELETON",
+    -5: "ESINGULAR_PIVOT", -6: "ESTATE", -7: "ECUDA", -8: "ENCCL", -9: "EOOM",
+}
+SYMBOLS = ["aifmm_build", "aifmm_set_compression_tol", "aifmm_factor", "aifmm_solve",
+           "aifmm_solve_host", "aifmm_free", "aifmm_last_error", "aifmm_set_stream",
+           "aifmm_get_tree", "aifmm_get_level_offsets", "aifmm_get_lists", "aifmm_get_colours",
+           "aifmm_get_ranks", "aifmm_stats", "aifmm_reset_counters", "aifmm_set_timing",
+           "aifmm_debug_inverse"]
+STAT_NAMES = ["build_ms", "factor_ms", "solve_ms", "levels", "top_size", "factor_flops",
+              "schur_flops", "schur_ms", "launches", "compressions", "max_rank", "device_bytes",
+              "schur_bytes", "schur_launches", "solve_bytes", "host_syncs"]
+
+
+class AIFMMError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libaifmm.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P, I, D, I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64
+    lib.aifmm_build.argtypes = [P, I64, I, I, P, I, D]
+    lib.aifmm_set_compression_tol.argtypes = [D]
+    lib.aifmm_factor.argtypes = []
+    lib.aifmm_solve.argtypes = [P, I]
+    lib.aifmm_solve_host.argtypes = [P, I]
+    lib.aifmm_free.restype = None
+    lib.aifmm_last_error.restype = ctypes.c_char_p
+    lib.aifmm_set_stream.argtypes = [P]
+    lib.aifmm_get_tree.argtypes = [P, P]
+    lib.aifmm_get_level_offsets.argtypes = [I, P]
+    lib.aifmm_get_lists.argtypes = [I, P, P, P, P]
+    lib.aifmm_get_colours.argtypes = [I, P]
+    lib.aifmm_get_ranks.argtypes = [I, I, P]
+    lib.aifmm_stats.argtypes = [P]
+    lib.aifmm_set_timing.argtypes = [I]
+    lib.aifmm_debug_inverse.argtypes = [P, I, I]
+    _lib = lib
+    return lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise AIFMMError(rc, _lib.aifmm_last_error().decode())
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def build(points, kernel_id: int, kparams, leaf_size: int, tol: float):
+    """points: torch.cuda float64 tensor (n, d), any layout (made contiguous)."""
+    import torch
+    lib = load()
+    if not (isinstance(points, torch.Tensor) and points.is_cuda):
+        raise TypeError("points must be a CUDA tensor (device memory)")
+    pts = points.to(torch.float64).contiguous()
+    kp = np.asarray(kparams, dtype=np.float64)
+    _check(lib.aifmm_build(ctypes.c_void_p(pts.data_ptr()), pts.shape[0], pts.shape[1], int(kernel_id),
+                           _ptr(kp), int(leaf_size), float(tol)))
+
+
+def set_compression_tol(tol_c: float):
+    _check(load().aifmm_set_compression_tol(float(tol_c)))
+
+
+def factor():
+    _check(load().aifmm_factor())
+
+
+def solve(B):
+    """B: torch.cuda float64 (n,) or (n, nrhs). Returns X with the same shape (new tensor)."""
+    import torch
+    lib = load()
+    one = B.dim() == 1
+    Bm = B[:, None] if one else B
+    Bc = Bm.to(torch.float64).t().contiguous()        # (nrhs, n) row-major == (n, nrhs) column-major
+    _check(lib.aifmm_solve(ctypes.c_void_p(Bc.data_ptr()), Bc.shape[0]))
+    X = Bc.t()
+    return X[:, 0] if one else X
+
+
+def solve_host(B: np.ndarray) -> np.ndarray:
+    """End-to-end path: host B (n,) or (n, nrhs) -> host X (copies inside the library)."""
+    lib = load()
+    one = B.ndim == 1
+    Bf = np.asfortranarray(np.array(B[:, None] if one else B, dtype=np.float64))
+    _check(lib.aifmm_solve_host(_ptr(Bf), Bf.shape[1]))
+    return Bf[:, 0] if one else Bf
+
+
+def free():
+    load().aifmm_free()
+
+
+def get_tree(n: int):
+    lib = load()
+    perm = np.zeros(n, dtype=np.int64)
+    L = ctypes.c_int(0)
+    _check(lib.aifmm_get_tree(_ptr(perm), ctypes.byref(L)))
+    return perm, L.value
+
+
+def get_level_offsets(level: int, d: int):
+    off = np.zeros((1 << (d * level)) + 1, dtype=np.int64)
+    _check(load().aifmm_get_level_offsets(level, _ptr(off)))
+    return off
+
+
+def get_lists(level: int, d: int):
+    lib = load()
+    nb = 1 << (d * level)
+    nptr = np.zeros(nb + 1, dtype=np.int32)
+    iptr = np.zeros(nb + 1, dtype=np.int32)
+    _check(lib.aifmm_get_lists(level, _ptr(nptr), None, _ptr(iptr), None))
+    nidx = np.zeros(max(int(nptr[-1]), 1), dtype=np.int32)
+    iidx = np.zeros(max(int(iptr[-1]), 1), dtype=np.int32)
+    _check(lib.aifmm_get_lists(level, _ptr(nptr), _ptr(nidx), _ptr(iptr), _ptr(iidx)))
+    return nptr, nidx[:nptr[-1]], iptr, iidx[:iptr[-1]]
+
+
+def get_colours(level: int, d: int):
+    col = np.zeros(1 << (d * level), dtype=np.int32)
+    _check(load().aifmm_get_colours(level, _ptr(col)))
+    return col
+
+
+def get_ranks(level: int, d: int, which: int = 0):
+    r = np.zeros(1 << (d * level), dtype=np.int32)
+    _check(load().aifmm_get_ranks(level, which, _ptr(r)))
+    return r
+
+
+def stats() -> dict:
+    out = np.zeros(16, dtype=np.float64)
+    _check(load().aifmm_stats(_ptr(out)))
+    return dict(zip(STAT_NAMES, out.tolist()))
+
+
+def reset_counters():
+    _check(load().aifmm_reset_counters())
+
+
+def set_timing(on: bool):
+    _check(load().aifmm_set_timing(1 if on else 0))
+
+
+def set_stream(stream_ptr: int):
+    _check(load().aifmm_set_stream(ctypes.c_void_p(stream_ptr)))
+
+
+def debug_inverse(M):
+    """In-place GPU inverse of a square CUDA float64 tensor (test hook); returns the inverse."""
+    import torch
+    Mc = M.to(torch.float64).t().contiguous()   # column-major storage of M
+    _check(load().aifmm_debug_inverse(ctypes.c_void_p(Mc.data_ptr()), Mc.shape[0], Mc.shape[0]))
+    return Mc.t()

@@ -1,0 +1,1481 @@
+// aifmm.cu — libaifmm host orchestrator and C-ABI (include/aifmm.h).
+//
+// The host plans; every floating-point step runs in the batched sm_100a kernels of
+// dense_kernels.cu / tree_kernels.cu / nnca_kernels.cu.  The host only handles integers:
+// tree metadata, lists, colours, ranks (read back after the kernels that decide them),
+// block offsets and task lists.
+//
+//   build  : G1 tree, G2 lists + colours, G3/G4 NNCA
+//   factor : per level L..2 (Alg. 3): setup / level transition,
+//            orthonormalisation (R13), per colour: compression + redirection of the pending
+//            far fill-ins (§3.2.1-3.2.3), batched pivot inverses and Schur updates (P:724-729,
+//            Table 4); top dense solve
+//   solve  : Algorithm 4 replaying the records on nrhs columns.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+
+#include "runtime.cuh"
+
+namespace aifmm {
+
+long long g_launches = 0;
+
+// tree launchers
+void tree_minmax(const double* pts, long long n, int d, double* part, int nparts, int* nonfinite, double* root, cudaStream_t s);
+void tree_coords(const double* pts, long long n, int d, const double* root, int* kc, cudaStream_t s);
+void tree_keys(const int* kc, long long n, int d, int l, int* key, cudaStream_t s);
+void tree_hist(const int* key, long long n, int* cnt, cudaStream_t s);
+void tree_max(const int* a, int n, int* out, cudaStream_t s);
+void tree_scan(const int* cnt, int nb, long long* off, cudaStream_t s);
+void tree_scatter(const int* key, long long n, const long long* off, int* cursor, int* perm, cudaStream_t s);
+void tree_segsort(const long long* off, int nb, int maxlen, int* perm, cudaStream_t s);
+void tree_gather(const double* pts, const int* perm, long long n, int d, double* sorted, cudaStream_t s);
+void tree_level_offsets(const long long* offL, int shift, int nb_l, long long* offl, cudaStream_t s);
+void tree_lists(const long long* offl, int l, int d, int ncap, int icap, int* ncnt, int* nidx, int* icnt, int* iidx, cudaStream_t s);
+void tree_colour(const long long* offl, int nb, int ncap, const int* ncnt, const int* nidx, int* col, cudaStream_t s);
+
+struct AcaTask {
+  const int* R;
+  const int* frange;
+  int nR, nfr, nF, kmax;
+  double* Uw;
+  double* Vw;
+  unsigned char* rused;
+  unsigned char* cused;
+  int* rank;
+  int* rpiv;
+  int* cpiv;
+};
+void launch_aca(const AcaTask* t, int ntasks, const double* pts, KernelParams kp, double eps, cudaStream_t s);
+
+// small integer kernels
+__global__ void iota_kernel(int* dst, long long n, int base) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = base + (int)i;
+}
+__global__ void icopy_kernel(const int* src, int* dst, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+// rows permutation of an N x nrhs column-major matrix: dst[j,:] = src[perm[j],:] (gather) or
+// dst[perm[j],:] = src[j,:] (scatter)
+__global__ void permute_rows_kernel(const double* src, double* dst, const int* perm, long long n, int nrhs, int scatter) {
+  const long long tot = n * nrhs;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long j = e % n, c = e / n;
+    if (scatter) dst[c * n + perm[j]] = src[c * n + j];
+    else dst[c * n + j] = src[c * n + perm[j]];
+  }
+}
+__global__ void finite_kernel(const double* a, long long n, int* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(a[i])) *flag = 1;
+}
+static int gsz(long long n) { return (int)std::min<long long>(std::max<long long>((n + 255) / 256, 1), 148 * 8); }
+
+// ------------------------------------------------------------------------------------ context
+struct Rec {
+  double* G = nullptr;
+  int m = 0, k = 0;
+  std::vector<std::pair<int, Blk>> R, C;   // (partner, block) as they were at elimination
+  std::vector<char> Rkind_y, Ckind_z;      // R: column was y_q (q eliminated); C: row was Z_p
+};
+
+struct NLevel {        // NNCA per level
+  std::vector<int> k, nR;              // by box id
+  std::vector<long long> Roff, Uoff, skoff;
+  int* dR = nullptr;                   // candidate rows (concatenated)
+  int* dsk = nullptr;                  // skeletons (concatenated, by skoff)
+  int* dfp = nullptr;                  // far pivots
+  double* dU = nullptr;                // compact U (nR x k, ld nR) at Uoff
+};
+
+struct FLevel {
+  int l = 0, nb = 0;
+  std::vector<int> boxes;
+  std::vector<int> m, k, kP;           // kP: columns of Ud (parent NNCA rank)
+  std::vector<double*> U, V, Ud, Vd;   // capacity: U,V m x m; Ud,Vd m x kP (ld m)
+  std::vector<char> E;
+  std::unordered_map<long long, Blk> nearb;   // current version of near blocks
+  std::unordered_map<long long, Blk> A, F;    // far M2L (cap m_p x m_q), far fill (dist-2)
+  std::set<std::pair<int, int>> pending;
+  std::vector<Rec> rec;
+  std::vector<int> xoff;               // row offset of child c (level l+1 id) inside its parent's x
+  std::vector<long long> xrow, zrow;   // solve layout
+  long long Xtot = 0, Ztot = 0;
+  long long key(int p, int q) const { return (long long)p * nb + q; }
+};
+
+struct Ctx {
+  cudaStream_t s = nullptr;
+  bool own_stream = false;
+  Uploader up;
+  DevPool persist{(size_t)512 << 20}, work{(size_t)256 << 20}, buildp{(size_t)256 << 20};
+  int d = 0, kid = 0, leaf = 0, L = 0;
+  long long n = 0;
+  KernelParams kp{};
+  double tol = 0, tol_c = -1, tol_c_user = -1;
+  double* pts = nullptr;                   // sorted points (device)
+  int* perm = nullptr;                     // device int32
+  int* dflag = nullptr;                    // device int error flag
+  std::vector<std::vector<long long>> off; // host, per level
+  std::vector<std::vector<int>> ncnt, nidx, icnt, iidx, col;
+  int ncap = 0, icap = 0;
+  std::vector<NLevel> nn;
+  std::vector<FLevel> fl;
+  double* topinv = nullptr;
+  int topn = 0;
+  std::vector<long long> topoff;
+  bool built = false, factored = false;
+  double stats[AIFMM_NSTATS] = {0};
+  FlopCounter fc_all, fc_schur;
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  // accessors
+  bool nonempty(int l, int b) const { return off[l][b + 1] > off[l][b]; }
+  int count(int l, int b) const { return (int)(off[l][b + 1] - off[l][b]); }
+  const int* nlist(int l, int b, int* cnt) const { *cnt = ncnt[l][b]; return &nidx[l][(size_t)b * ncap]; }
+  const int* ilist(int l, int b, int* cnt) const { *cnt = icnt[l][b]; return &iidx[l][(size_t)b * icap]; }
+  int cheb(int l, int a, int b) const {
+    int r = 0;
+    for (int ax = 0; ax < d; ++ax) {
+      int ca = 0, cb = 0;
+      for (int bit = 0; bit < l; ++bit) {
+        ca |= ((a >> (bit * d + ax)) & 1) << bit;
+        cb |= ((b >> (bit * d + ax)) & 1) << bit;
+      }
+      r = std::max(r, std::abs(ca - cb));
+    }
+    return r;
+  }
+};
+
+// Optional phase profile (AIFMM_PROFILE=1): synchronises at phase boundaries and prints a
+// breakdown to stderr at the end of factor / solve.  Off by default (no extra syncs).
+struct Prof {
+  bool on = false;
+  std::map<std::string, double> ms;
+  std::chrono::steady_clock::time_point t0;
+  cudaStream_t s = nullptr;
+  void begin(cudaStream_t st) { if (!on) return; s = st; cudaStreamSynchronize(s); t0 = std::chrono::steady_clock::now(); }
+  void end(const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    ms[name] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  void dump(const char* title) {
+    if (!on) return;
+    fprintf(stderr, "[aifmm profile] %s:", title);
+    for (auto& kv : ms) fprintf(stderr, " %s=%.2fms", kv.first.c_str(), kv.second);
+    fprintf(stderr, "\n");
+    ms.clear();
+  }
+};
+static Prof g_prof;
+
+static Ctx* g_ctx = nullptr;
+static std::string g_err;
+
+static Ctx& ctx() {
+  if (!g_ctx) g_ctx = new Ctx();
+  if (!g_ctx->s) {
+    AIFMM_CUDA(cudaStreamCreateWithFlags(&g_ctx->s, cudaStreamNonBlocking));
+    g_ctx->own_stream = true;
+    g_ctx->up.init(g_ctx->s);
+    AIFMM_CUDA(cudaMalloc(&g_ctx->dflag, 64));
+  }
+  return *g_ctx;
+}
+
+static void check_flag(Ctx& c, int code, const char* msg) {
+  int h = 0;
+  AIFMM_CUDA(cudaMemcpyAsync(&h, c.dflag, sizeof(int), cudaMemcpyDeviceToHost, c.s));
+  c.up.sync();
+  if (h) {
+    AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
+    throw Error(code, msg);
+  }
+}
+
+template <class T>
+static std::vector<T> d2h(Ctx& c, const T* d, size_t n) {
+  std::vector<T> h(n);
+  if (n) AIFMM_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, c.s));
+  c.up.sync();
+  return h;
+}
+
+// ------------------------------------------------------------------------------------ build
+static void build_tree(Ctx& c, const double* user_pts) {
+  const long long n = c.n;
+  const int d = c.d;
+  DevPool& P = c.buildp;
+  double* part = P.d(6 * 148);
+  double* root = P.d(4);
+  int* kc = P.i((size_t)n * d);
+  int* key = P.i(n);
+  AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, 64, c.s));
+  tree_minmax(user_pts, n, d, part, 148, c.dflag, root, c.s);
+  check_flag(c, AIFMM_ENONFINITE, "non-finite point coordinates");
+  tree_coords(user_pts, n, d, root, kc, c.s);
+  int* dmax = P.i(1);
+  int L = -1;
+  for (int l = 2; l <= 20; ++l) {
+    AIFMM_REQUIRE(d * l <= 24, AIFMM_EINVALID_ARG,
+                  "cannot subdivide: coincident points or a tree deeper than 2^24 boxes per level");
+    const int nb = 1 << (d * l);
+    int* cnt = c.work.i(nb);
+    AIFMM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * nb, c.s));
+    AIFMM_CUDA(cudaMemsetAsync(dmax, 0, sizeof(int), c.s));
+    tree_keys(kc, n, d, l, key, c.s);
+    tree_hist(key, n, cnt, c.s);
+    tree_max(cnt, nb, dmax, c.s);
+    int mx = d2h(c, dmax, 1)[0];
+    c.work.reset();
+    if (mx <= c.leaf) { L = l; break; }
+  }
+  c.L = L;
+  const int nbL = 1 << (d * L);
+  int* cnt = P.i(nbL);
+  int* cursor = P.i(nbL);
+  long long* offL = static_cast<long long*>(P.alloc(sizeof(long long) * (nbL + 1)));
+  AIFMM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * nbL, c.s));
+  AIFMM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(int) * nbL, c.s));
+  tree_keys(kc, n, d, L, key, c.s);
+  tree_hist(key, n, cnt, c.s);
+  tree_scan(cnt, nbL, offL, c.s);
+  c.perm = static_cast<int*>(c.persist.alloc(sizeof(int) * n));
+  tree_scatter(key, n, offL, cursor, c.perm, c.s);
+  tree_segsort(offL, nbL, c.leaf, c.perm, c.s);
+  c.pts = c.persist.d((size_t)n * d);
+  tree_gather(user_pts, c.perm, n, d, c.pts, c.s);
+  // offsets per level + lists + colours
+  c.off.assign(L + 1, {});
+  c.ncnt.assign(L + 1, {});
+  c.nidx.assign(L + 1, {});
+  c.icnt.assign(L + 1, {});
+  c.iidx.assign(L + 1, {});
+  c.col.assign(L + 1, {});
+  c.ncap = (d == 2) ? 9 : 27;
+  c.icap = (d == 2) ? 27 : 189;
+  for (int l = 0; l <= L; ++l) {
+    const int nb = 1 << (d * l);
+    long long* offl = static_cast<long long*>(P.alloc(sizeof(long long) * (nb + 1)));
+    tree_level_offsets(offL, d * (L - l), nb, offl, c.s);
+    if (l >= 2) {
+      int* ncnt = P.i(nb);
+      int* nidx = P.i((size_t)nb * c.ncap);
+      int* icnt = P.i(nb);
+      int* iidx = P.i((size_t)nb * c.icap);
+      int* col = P.i(nb);
+      tree_lists(offl, l, d, c.ncap, c.icap, ncnt, nidx, icnt, iidx, c.s);
+      tree_colour(offl, nb, c.ncap, ncnt, nidx, col, c.s);
+      c.ncnt[l] = d2h(c, ncnt, nb);
+      c.nidx[l] = d2h(c, nidx, (size_t)nb * c.ncap);
+      c.icnt[l] = d2h(c, icnt, nb);
+      c.iidx[l] = d2h(c, iidx, (size_t)nb * c.icap);
+      c.col[l] = d2h(c, col, nb);
+    }
+    c.off[l] = d2h(c, offl, nb + 1);
+  }
+}
+
+static void build_nnca(Ctx& c) {
+  const int L = c.L;
+  c.nn.assign(L + 1, NLevel{});
+  const double eps = c.tol / 100.0;   // reading R18
+  for (int l = L; l >= 2; --l) {
+    NLevel& nl = c.nn[l];
+    const int nb = 1 << (c.d * l);
+    nl.k.assign(nb, 0);
+    nl.nR.assign(nb, 0);
+    nl.Roff.assign(nb + 1, 0);
+    std::vector<int> boxes;
+    for (int b = 0; b < nb; ++b)
+      if (c.nonempty(l, b)) boxes.push_back(b);
+    // candidate rows
+    for (int b = 0; b < nb; ++b) {
+      int r = 0;
+      if (c.nonempty(l, b)) {
+        if (l == L) r = c.count(l, b);
+        else
+          for (int ch = 0; ch < (1 << c.d); ++ch) r += c.nn[l + 1].k[(b << c.d) | ch];
+      }
+      nl.nR[b] = r;
+      nl.Roff[b + 1] = nl.Roff[b] + r;
+    }
+    nl.dR = c.persist.i(std::max<long long>(nl.Roff[nb], 1));
+    for (int b : boxes) {
+      if (!nl.nR[b]) continue;
+      if (l == L) {
+        LAUNCH(iota_kernel, gsz(nl.nR[b]), 256, 0, c.s, nl.dR + nl.Roff[b], (long long)nl.nR[b], (int)c.off[l][b]);
+      }
+    }
+    if (l < L) {
+      // concatenate children's skeletons (children are consecutive ids, so the concatenation
+      // of children's sk arrays in Morton order is one contiguous copy per parent)
+      const NLevel& cl = c.nn[l + 1];
+      for (int b : boxes) {
+        if (!nl.nR[b]) continue;
+        long long s0 = cl.skoff[(size_t)b << c.d];
+        LAUNCH(icopy_kernel, gsz(nl.nR[b]), 256, 0, c.s, cl.dsk + s0, nl.dR + nl.Roff[b], (long long)nl.nR[b]);
+      }
+    }
+    // far ranges per box
+    std::vector<int> fr;
+    std::vector<long long> froff(nb + 1, 0);
+    std::vector<int> nF(nb, 0);
+    for (int b = 0; b < nb; ++b) {
+      froff[b + 1] = froff[b];
+      if (!c.nonempty(l, b)) continue;
+      int ni;
+      const int* il = c.ilist(l, b, &ni);
+      for (int t = 0; t < ni; ++t) {
+        fr.push_back((int)c.off[l][il[t]]);
+        fr.push_back((int)c.off[l][il[t] + 1]);
+        nF[b] += c.count(l, il[t]);
+      }
+      froff[b + 1] += ni;
+    }
+    int* dfr = fr.empty() ? nullptr : c.up.put(fr);
+    // ACA in chunks bounded by workspace
+    int* drank = c.persist.i(nb);
+    AIFMM_CUDA(cudaMemsetAsync(drank, 0, sizeof(int) * nb, c.s));
+    std::vector<long long> kmaxv(nb, 0);
+    long long pivtot = 0;
+    std::vector<long long> pivoff(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) {
+      kmaxv[b] = std::min<long long>(nl.nR[b], nF[b]);
+      pivoff[b + 1] = pivoff[b] + kmaxv[b];
+    }
+    pivtot = pivoff[nb];
+    int* drp = c.persist.i(std::max<long long>(pivtot, 1));
+    int* dcp = c.persist.i(std::max<long long>(pivtot, 1));
+    const size_t budget = (size_t)6 << 30;
+    size_t i0 = 0;
+    while (i0 < boxes.size()) {
+      std::vector<AcaTask> tasks;
+      size_t ws = 0;
+      size_t i1 = i0;
+      c.work.reset();
+      while (i1 < boxes.size()) {
+        int b = boxes[i1];
+        size_t need = (size_t)kmaxv[b] * (nl.nR[b] + nF[b]) * 8 + nl.nR[b] + nF[b] + 1024;
+        if (!tasks.empty() && ws + need > budget) break;
+        ws += need;
+        if (kmaxv[b] > 0) {
+          AcaTask t{};
+          t.R = nl.dR + nl.Roff[b];
+          t.frange = dfr + 2 * froff[b];
+          t.nR = nl.nR[b];
+          t.nfr = (int)(froff[b + 1] - froff[b]);
+          AIFMM_REQUIRE(t.nfr <= 256, AIFMM_EINVALID_ARG, "too many far ranges");
+          t.nF = nF[b];
+          t.kmax = (int)kmaxv[b];
+          t.Uw = c.work.d((size_t)t.nR * t.kmax);
+          t.Vw = c.work.d((size_t)t.nF * t.kmax);
+          t.rused = static_cast<unsigned char*>(c.work.alloc(t.nR));
+          t.cused = static_cast<unsigned char*>(c.work.alloc(t.nF));
+          t.rank = drank + b;
+          t.rpiv = drp + pivoff[b];
+          t.cpiv = dcp + pivoff[b];
+          tasks.push_back(t);
+        }
+        ++i1;
+      }
+      if (!tasks.empty()) launch_aca(c.up.put(tasks), (int)tasks.size(), c.pts, c.kp, eps, c.s);
+      c.up.sync();
+      i0 = i1;
+    }
+    c.work.reset();
+    nl.k = d2h(c, drank, nb);
+    // skeleton / far-pivot arrays compacted by box
+    nl.skoff.assign(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) nl.skoff[b + 1] = nl.skoff[b] + nl.k[b];
+    nl.dsk = c.persist.i(std::max<long long>(nl.skoff[nb], 1));
+    nl.dfp = c.persist.i(std::max<long long>(nl.skoff[nb], 1));
+    for (int b : boxes) {
+      if (!nl.k[b]) continue;
+      LAUNCH(icopy_kernel, gsz(nl.k[b]), 256, 0, c.s, drp + pivoff[b], nl.dsk + nl.skoff[b], (long long)nl.k[b]);
+      LAUNCH(icopy_kernel, gsz(nl.k[b]), 256, 0, c.s, dcp + pivoff[b], nl.dfp + nl.skoff[b], (long long)nl.k[b]);
+    }
+    // operators: [A(fp,sk) | A(fp,R)] -> [I | X] by Gauss-Jordan (a solve, not an explicit
+    // inverse: A(fp,sk) can be ill-conditioned), U = X^T (R10: V = U)
+    nl.Uoff.assign(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) nl.Uoff[b + 1] = nl.Uoff[b] + (long long)nl.nR[b] * nl.k[b];
+    nl.dU = c.persist.d(std::max<long long>(nl.Uoff[nb], 1));
+    std::vector<KEvalTask> kt;
+    std::vector<GJTask> gs, gg;
+    long long smem_s = 0;
+    int nmax_g = 1;
+    CopyBatch cb;
+    int* dinfo = c.work.i(nb);
+    AIFMM_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int) * nb, c.s));
+    AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
+    for (int b : boxes) {
+      const int k = nl.k[b], nr = nl.nR[b];
+      if (!k) continue;
+      double* aug = c.work.d((size_t)k * (k + nr));
+      kt.push_back(KEvalTask{aug, k, k, k, nl.dfp + nl.skoff[b], nl.dsk + nl.skoff[b], 0, 0});
+      kt.push_back(KEvalTask{aug + (size_t)k * k, k, k, nr, nl.dfp + nl.skoff[b], nl.dR + nl.Roff[b], 0, 0});
+      const long long need = (long long)k * (k + nr) + k + k / 2 + 2;
+      if (need * 8 <= 160 * 1024) {
+        gs.push_back(GJTask{aug, k, k, k + nr, 0, dinfo + b});
+        smem_s = std::max(smem_s, need);
+      } else {
+        gg.push_back(GJTask{aug, k, k, k + nr, 0, dinfo + b});
+        nmax_g = std::max(nmax_g, k);
+      }
+      cb.copy(aug + (size_t)k * k, k, nl.dU + nl.Uoff[b], nr, nr, k, 1.0, /*trans=*/1);
+    }
+    if (!kt.empty()) {
+      launch_keval(c.up.put(kt), (int)kt.size(), 4, c.pts, c.kp, c.dflag, c.s);
+      if (!gs.empty()) launch_gj(c.up.put(gs), (int)gs.size(), (int)smem_s, 0, c.s);
+      if (!gg.empty()) launch_gj(c.up.put(gg), (int)gg.size(), -nmax_g, 0, c.s);
+      cb.run(c.up, c.s);
+    }
+    check_flag(c, AIFMM_ECOINCIDENT, "coincident points with a singular kernel");
+    std::vector<int> info = d2h(c, dinfo, nb);
+    for (int b : boxes)
+      if (nl.k[b] && info[b])
+        throw Error(AIFMM_ESINGULAR_SKELETON, "NNCA skeleton block singular at level " + std::to_string(l) +
+                                                  " box " + std::to_string(b));
+    c.work.reset();
+  }
+}
+
+// ------------------------------------------------------------------------------------ factor
+static inline int live(const FLevel& f, int b) { return f.E[b] ? f.k[b] : f.m[b]; }
+
+static void setup_level(Ctx& c, int l) {
+  FLevel& f = c.fl[l];
+  const int d = c.d, nb = 1 << (d * l);
+  f.l = l;
+  f.nb = nb;
+  f.boxes.clear();
+  for (int b = 0; b < nb; ++b)
+    if (c.nonempty(l, b)) f.boxes.push_back(b);
+  f.m.assign(nb, 0);
+  f.k.assign(nb, 0);
+  f.kP.assign(nb, 0);
+  f.U.assign(nb, nullptr);
+  f.V.assign(nb, nullptr);
+  f.Ud.assign(nb, nullptr);
+  f.Vd.assign(nb, nullptr);
+  f.E.assign(nb, 0);
+  f.rec.assign(nb, Rec{});
+  f.nearb.clear();
+  f.A.clear();
+  f.F.clear();
+  f.pending.clear();
+  const NLevel& nl = c.nn[l];
+  FLevel* prev = (l < c.L) ? &c.fl[l + 1] : nullptr;
+  if (prev) prev->xoff.assign(1 << (d * (l + 1)), 0);
+  for (int b : f.boxes) {
+    if (l == c.L) f.m[b] = c.count(l, b);
+    else {
+      int o = 0;
+      for (int ch = 0; ch < (1 << d); ++ch) {
+        int cb = (b << d) | ch;
+        if (!c.nonempty(l + 1, cb)) continue;
+        prev->xoff[cb] = o;
+        o += prev->k[cb];
+      }
+      f.m[b] = o;
+    }
+    f.k[b] = nl.k[b];
+    f.kP[b] = (l > 2) ? c.nn[l - 1].k[b >> d] : 0;
+  }
+  // zero-initialised capacity storage: U, V, Ud, Vd, far A, far F
+  size_t zbytes = 0;
+  auto rnd = [](size_t x) { return (x * 8 + 255) & ~(size_t)255; };
+  for (int b : f.boxes) {
+    zbytes += 2 * rnd((size_t)f.m[b] * f.m[b]) + 2 * rnd((size_t)f.m[b] * f.kP[b]);
+    int ni;
+    const int* il = c.ilist(l, b, &ni);
+    for (int t = 0; t < ni; ++t) {
+      zbytes += rnd((size_t)f.m[b] * f.m[il[t]]);
+      if (c.cheb(l, b, il[t]) == 2) zbytes += rnd((size_t)f.m[b] * f.m[il[t]]);
+    }
+  }
+  char* z = static_cast<char*>(c.persist.alloc(std::max<size_t>(zbytes, 256)));
+  AIFMM_CUDA(cudaMemsetAsync(z, 0, zbytes, c.s));
+  size_t zo = 0;
+  auto carve = [&](size_t nel) { double* p = reinterpret_cast<double*>(z + zo); zo += rnd(nel); return p; };
+  for (int b : f.boxes) {
+    f.U[b] = carve((size_t)f.m[b] * f.m[b]);
+    f.V[b] = carve((size_t)f.m[b] * f.m[b]);
+    f.Ud[b] = carve((size_t)f.m[b] * f.kP[b]);
+    f.Vd[b] = carve((size_t)f.m[b] * f.kP[b]);
+    int ni;
+    const int* il = c.ilist(l, b, &ni);
+    for (int t = 0; t < ni; ++t) {
+      int q = il[t];
+      f.A[f.key(b, q)] = Blk{carve((size_t)f.m[b] * f.m[q]), std::max(f.m[b], 1), f.k[b], f.k[q]};
+      if (c.cheb(l, b, q) == 2) f.F[f.key(b, q)] = Blk{carve((size_t)f.m[b] * f.m[q]), std::max(f.m[b], 1), 0, 0};
+    }
+  }
+  // fills
+  CopyBatch cb;
+  std::vector<KEvalTask> kt;
+  for (int b : f.boxes) {
+    const int m = f.m[b], k = f.k[b];
+    if (l == c.L) {
+      cb.copy(nl.dU + nl.Uoff[b], nl.nR[b], f.U[b], m, m, k);
+      cb.copy(nl.dU + nl.Uoff[b], nl.nR[b], f.V[b], m, m, k);
+    } else {
+      for (int ch = 0; ch < (1 << d); ++ch) {
+        int cbx = (b << d) | ch;
+        if (!c.nonempty(l + 1, cbx)) continue;
+        cb.copy(prev->Ud[cbx], std::max(prev->m[cbx], 1), f.U[b] + prev->xoff[cbx], m, prev->k[cbx], k);
+        cb.copy(prev->Vd[cbx], std::max(prev->m[cbx], 1), f.V[b] + prev->xoff[cbx], m, prev->k[cbx], k);
+      }
+    }
+    if (l > 2) {
+      // L2L / M2M: rows of the parent's NNCA operator belonging to b
+      const int P = b >> d;
+      const NLevel& pl = c.nn[l - 1];
+      int r0 = 0;
+      for (int ch = 0; ch < (b & ((1 << d) - 1)); ++ch) r0 += nl.k[(P << d) | ch];
+      cb.copy(pl.dU + pl.Uoff[P] + r0, pl.nR[P], f.Ud[b], std::max(m, 1), k, f.kP[b]);
+      cb.copy(pl.dU + pl.Uoff[P] + r0, pl.nR[P], f.Vd[b], std::max(m, 1), k, f.kP[b]);
+    }
+    // near blocks (current version = X_p x x_q)
+    int nn_;
+    const int* nbl = c.nlist(l, b, &nn_);
+    for (int t = 0; t < nn_; ++t) {
+      int q = nbl[t];
+      Blk blk{c.persist.d(std::max<size_t>((size_t)m * f.m[q], 1)), std::max(m, 1), m, f.m[q]};
+      f.nearb[f.key(b, q)] = blk;
+      if (l == c.L) {
+        kt.push_back(KEvalTask{blk.p, blk.ld, m, f.m[q], nullptr, nullptr, (int)c.off[l][b], (int)c.off[l][q]});
+      } else {
+        for (int ch = 0; ch < (1 << d); ++ch) {
+          int c1 = (b << d) | ch;
+          if (!c.nonempty(l + 1, c1)) continue;
+          for (int ch2 = 0; ch2 < (1 << d); ++ch2) {
+            int c2 = (q << d) | ch2;
+            if (!c.nonempty(l + 1, c2)) continue;
+            auto it = prev->nearb.find(prev->key(c1, c2));
+            const Blk& src = (it != prev->nearb.end()) ? it->second : prev->A.at(prev->key(c1, c2));
+            cb.copy(src.p, src.ld, blk.p + (size_t)prev->xoff[c2] * blk.ld + prev->xoff[c1], blk.ld,
+                    prev->k[c1], prev->k[c2]);
+          }
+        }
+      }
+    }
+    // M2L A(sk b, sk q)
+    int ni;
+    const int* il = c.ilist(l, b, &ni);
+    for (int t = 0; t < ni; ++t) {
+      int q = il[t];
+      const Blk& a = f.A[f.key(b, q)];
+      if (f.k[b] && f.k[q])
+        kt.push_back(KEvalTask{a.p, a.ld, f.k[b], f.k[q], nl.dsk + nl.skoff[b], nl.dsk + nl.skoff[q], 0, 0});
+    }
+  }
+  AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
+  cb.run(c.up, c.s);
+  if (!kt.empty()) launch_keval(c.up.put(kt), (int)kt.size(), 4, c.pts, c.kp, c.dflag, c.s);
+}
+
+// R13: U_b = Q T, V_b = Q' T'; rows of Z_b <- T (.), columns of y_b <- (.) T'^T
+static void orthonormalise(Ctx& c, FLevel& f) {
+  const int l = f.l;
+  std::vector<double*> Uold(f.nb, nullptr), Vold(f.nb, nullptr), T(f.nb, nullptr), T2(f.nb, nullptr);
+  CopyBatch cb;
+  std::vector<PqrTask> pq;
+  size_t smem = 0;
+  for (int b : f.boxes) {
+    const int m = f.m[b], k = f.k[b];
+    if (!k) continue;
+    Uold[b] = c.work.d((size_t)m * k);
+    Vold[b] = c.work.d((size_t)m * k);
+    double* wu = c.work.d((size_t)m * k);
+    double* wv = c.work.d((size_t)m * k);
+    cb.copy(f.U[b], m, Uold[b], m, m, k);
+    cb.copy(f.U[b], m, wu, m, m, k);
+    cb.copy(f.V[b], m, Vold[b], m, m, k);
+    cb.copy(f.V[b], m, wv, m, m, k);
+    pq.push_back(PqrTask{wu, f.U[b], m, m, m, k, 0, k, k, 0, nullptr, 0.0, nullptr, nullptr});
+    pq.push_back(PqrTask{wv, f.V[b], m, m, m, k, 0, k, k, 0, nullptr, 0.0, nullptr, nullptr});
+    smem = std::max(smem, (size_t)k + m + k);
+  }
+  cb.run(c.up, c.s);
+  if (!pq.empty()) launch_pqr(c.up.put(pq), (int)pq.size(), smem, c.s);
+  GemmBatch g;
+  for (int b : f.boxes) {
+    const int m = f.m[b], k = f.k[b];
+    if (!k) continue;
+    T[b] = c.work.d((size_t)k * k);
+    T2[b] = c.work.d((size_t)k * k);
+    g.task(T[b], k, k, k, 0.0);
+    g.term(1.0, f.U[b], m, 1, Uold[b], m, 0, m);
+    g.task(T2[b], k, k, k, 0.0);
+    g.term(1.0, f.V[b], m, 1, Vold[b], m, 0, m);
+  }
+  g.run(c.up, c.s, &c.fc_all);
+  // Ud <- T Ud, Vd <- T' Vd ; A_pq <- T_p A_pq T'_q^T
+  std::vector<double*> udc(f.nb, nullptr), vdc(f.nb, nullptr);
+  std::unordered_map<long long, double*> tmpA;
+  for (int b : f.boxes) {
+    const int m = f.m[b], k = f.k[b];
+    if (!k) continue;
+    if (f.kP[b]) {
+      udc[b] = c.work.d((size_t)k * f.kP[b]);
+      vdc[b] = c.work.d((size_t)k * f.kP[b]);
+      cb.copy(f.Ud[b], m, udc[b], k, k, f.kP[b]);
+      cb.copy(f.Vd[b], m, vdc[b], k, k, f.kP[b]);
+    }
+    int ni;
+    const int* il = c.ilist(l, b, &ni);
+    for (int t = 0; t < ni; ++t) {
+      int q = il[t];
+      if (!f.k[q]) continue;
+      double* tp = c.work.d((size_t)k * f.k[q]);
+      tmpA[f.key(b, q)] = tp;
+      const Blk& a = f.A[f.key(b, q)];
+      g.task(tp, k, k, f.k[q], 0.0);
+      g.term(1.0, a.p, a.ld, 0, T2[q], f.k[q], 1, f.k[q]);
+    }
+  }
+  cb.run(c.up, c.s);
+  g.run(c.up, c.s, &c.fc_all);
+  for (int b : f.boxes) {
+    const int m = f.m[b], k = f.k[b];
+    if (!k) continue;
+    if (f.kP[b]) {
+      g.task(f.Ud[b], m, k, f.kP[b], 0.0);
+      g.term(1.0, T[b], k, 0, udc[b], k, 0, k);
+      g.task(f.Vd[b], m, k, f.kP[b], 0.0);
+      g.term(1.0, T2[b], k, 0, vdc[b], k, 0, k);
+    }
+    int ni;
+    const int* il = c.ilist(l, b, &ni);
+    for (int t = 0; t < ni; ++t) {
+      int q = il[t];
+      if (!f.k[q]) continue;
+      const Blk& a = f.A[f.key(b, q)];
+      g.task(a.p, a.ld, k, f.k[q], 0.0);
+      g.term(1.0, T[b], k, 0, tmpA[f.key(b, q)], k, 0, k);
+    }
+  }
+  g.run(c.up, c.s, &c.fc_all);
+  c.up.sync();
+  c.work.reset();
+}
+
+// Alg. 3 lines P:1118-1129 for the pending pairs S (colour-batched, R12; R14, R15)
+static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& S) {
+  std::map<int, std::vector<int>> part;
+  for (auto& pr : S) {
+    part[pr.first].push_back(pr.second);
+    part[pr.second].push_back(pr.first);
+  }
+  std::vector<int> aff;
+  for (auto& kv : part) {
+    std::sort(kv.second.begin(), kv.second.end());
+    if (!f.E[kv.first]) aff.push_back(kv.first);
+  }
+  const int na = (int)aff.size();
+  if (!na) return;
+  struct Side { double* W; int nc; };
+  std::vector<Side> su(na), sv(na);
+  double* dnorm = c.work.d(2 * na);
+  int* dt = c.work.i(4 * na);
+  CopyBatch cb;
+  std::vector<NormTask> nt;
+  for (int a = 0; a < na; ++a) {
+    int b = aff[a];
+    const int m = f.m[b];
+    int ncu = 0, ncv = 0;
+    for (int q : part[b]) { ncu += live(f, q); ncv += live(f, q); }
+    su[a] = Side{c.work.d((size_t)m * std::max(ncu, 1)), ncu};
+    sv[a] = Side{c.work.d((size_t)m * std::max(ncv, 1)), ncv};
+    int ou = 0, ov = 0;
+    for (int q : part[b]) {
+      const Blk& fb = f.F.at(f.key(b, q));   // row X_b, column of q
+      cb.copy(fb.p, fb.ld, su[a].W + (size_t)ou * m, m, m, live(f, q));
+      ou += live(f, q);
+      const Blk& gb = f.F.at(f.key(q, b));   // row of q, column x_b -> transposed
+      cb.copy(gb.p, gb.ld, sv[a].W + (size_t)ov * m, m, m, live(f, q), 1.0, /*trans=*/1);
+      ov += live(f, q);
+    }
+    nt.push_back(NormTask{su[a].W, m, m, ncu, dnorm + 2 * a});
+    nt.push_back(NormTask{sv[a].W, m, m, ncv, dnorm + 2 * a + 1});
+  }
+  cb.run(c.up, c.s);
+  launch_norm(c.up.put(nt), (int)nt.size(), c.s);
+  // projection W -= B (B^T W)
+  GemmBatch g;
+  std::vector<double*> tu(na), tv(na);
+  for (int a = 0; a < na; ++a) {
+    int b = aff[a];
+    const int m = f.m[b], k = f.k[b];
+    if (!k) continue;
+    tu[a] = c.work.d((size_t)k * std::max(su[a].nc, 1));
+    tv[a] = c.work.d((size_t)k * std::max(sv[a].nc, 1));
+    g.task(tu[a], k, k, su[a].nc, 0.0);
+    g.term(1.0, f.U[b], m, 1, su[a].W, m, 0, m);
+    g.task(tv[a], k, k, sv[a].nc, 0.0);
+    g.term(1.0, f.V[b], m, 1, sv[a].W, m, 0, m);
+  }
+  g.run(c.up, c.s, &c.fc_all);
+  for (int a = 0; a < na; ++a) {
+    int b = aff[a];
+    const int m = f.m[b], k = f.k[b];
+    if (!k) continue;
+    g.task(su[a].W, m, m, su[a].nc, 1.0);
+    g.term(-1.0, f.U[b], m, 0, tu[a], k, 0, k);
+    g.task(sv[a].W, m, m, sv[a].nc, 1.0);
+    g.term(-1.0, f.V[b], m, 0, tv[a], k, 0, k);
+  }
+  g.run(c.up, c.s, &c.fc_all);
+  // phase A: truncated pivoted QR on both sides
+  std::vector<PqrTask> pq;
+  size_t smem = 0;
+  for (int a = 0; a < na; ++a) {
+    int b = aff[a];
+    const int m = f.m[b], k = f.k[b];
+    pq.push_back(PqrTask{su[a].W, f.U[b], m, m, m, su[a].nc, k, 0, m - k, 0, dnorm + 2 * a, c.tol_c, dt + 4 * a, dt + 4 * a + 1});
+    pq.push_back(PqrTask{sv[a].W, f.V[b], m, m, m, sv[a].nc, k, 0, m - k, 0, dnorm + 2 * a + 1, c.tol_c, dt + 4 * a + 2, dt + 4 * a + 3});
+    smem = std::max(smem, (size_t)std::max(su[a].nc, sv[a].nc) + m + m);
+  }
+  launch_pqr(c.up.put(pq), (int)pq.size(), smem, c.s);
+  std::vector<int> th = d2h(c, dt, 4 * na);
+  std::vector<int> tgt(na), hu(na), hv(na);
+  pq.clear();
+  smem = 0;
+  for (int a = 0; a < na; ++a) {
+    int b = aff[a];
+    const int m = f.m[b], k = f.k[b];
+    hu[a] = th[4 * a + 1];
+    hv[a] = th[4 * a + 3];
+    tgt[a] = std::min(std::max(th[4 * a], th[4 * a + 2]), m - k);
+    if (hu[a] < tgt[a])
+      pq.push_back(PqrTask{su[a].W, f.U[b], m, m, m, su[a].nc, k + hu[a], tgt[a] - hu[a], tgt[a] - hu[a], 0, nullptr, 0.0,
+                           nullptr, dt + 4 * a + 1});
+    if (hv[a] < tgt[a])
+      pq.push_back(PqrTask{sv[a].W, f.V[b], m, m, m, sv[a].nc, k + hv[a], tgt[a] - hv[a], tgt[a] - hv[a], 0, nullptr, 0.0,
+                           nullptr, dt + 4 * a + 3});
+    smem = std::max(smem, (size_t)std::max(su[a].nc, sv[a].nc) + m + m);
+  }
+  std::vector<int> haveU = hu, haveV = hv;
+  if (!pq.empty()) {
+    // phase B: continue the shorter side past its truncation point (R15)
+    launch_pqr(c.up.put(pq), (int)pq.size(), smem, c.s);
+    th = d2h(c, dt, 4 * na);
+    for (int a = 0; a < na; ++a) {
+      if (hu[a] < tgt[a]) haveU[a] = hu[a] + th[4 * a + 1];
+      if (hv[a] < tgt[a]) haveV[a] = hv[a] + th[4 * a + 3];
+    }
+    // sides still short (candidates exhausted): projected identity columns
+    std::vector<PqrTask> pi;
+    std::vector<std::pair<int, int>> who;
+    size_t smem2 = 0;
+    for (int a = 0; a < na; ++a) {
+      int b = aff[a];
+      const int m = f.m[b], k = f.k[b];
+      for (int side = 0; side < 2; ++side) {
+        const int have = side ? haveV[a] : haveU[a];
+        if (have >= tgt[a]) continue;
+        double* Bm = side ? f.V[b] : f.U[b];
+        const int kb = k + have;
+        double* WI = c.work.d((size_t)m * m);
+        double* tmp = c.work.d((size_t)std::max(kb, 1) * m);
+        CopyBatch z;
+        z.fill(WI, m, m, m, 0.0);
+        z.copy(nullptr, 0, WI, m + 1, 1, m, 1.0, 0, 1);   // + I (walk the diagonal)
+        z.run(c.up, c.s);
+        GemmBatch gi;
+        gi.task(WI, m, m, m, 1.0);
+        gi.term(-1.0, Bm, m, 0, Bm, m, 1, kb);
+        gi.run(c.up, c.s);
+        gi.task(tmp, kb, kb, m, 0.0);
+        gi.term(1.0, Bm, m, 1, WI, m, 0, m);
+        gi.run(c.up, c.s);
+        gi.task(WI, m, m, m, 1.0);
+        gi.term(-1.0, Bm, m, 0, tmp, kb, 0, kb);
+        gi.run(c.up, c.s);
+        pi.push_back(PqrTask{WI, Bm, m, m, m, m, kb, tgt[a] - have, tgt[a] - have, 0, nullptr, 0.0, nullptr,
+                             dt + 4 * a + 1 + 2 * side});
+        who.push_back({a, side});
+        smem2 = std::max(smem2, (size_t)m + m + m);
+      }
+    }
+    if (!pi.empty()) {
+      launch_pqr(c.up.put(pi), (int)pi.size(), smem2, c.s);
+      th = d2h(c, dt, 4 * na);
+      for (auto& w : who) {
+        if (w.second) haveV[w.first] += th[4 * w.first + 3];
+        else haveU[w.first] += th[4 * w.first + 1];
+      }
+    }
+  }
+  for (int a = 0; a < na; ++a)
+    AIFMM_REQUIRE(haveU[a] == tgt[a] && haveV[a] == tgt[a], AIFMM_ESINGULAR_PIVOT, "rank equalisation failed");
+  // new ranks
+  for (int a = 0; a < na; ++a) {
+    int b = aff[a];
+    f.k[b] += tgt[a];
+    c.stats[AIFMM_STAT_COMPRESSIONS] += 1;
+  }
+  for (auto& kv : f.A) {
+    int p = (int)(kv.first / f.nb), q = (int)(kv.first % f.nb);
+    kv.second.rows = f.k[p];
+    kv.second.cols = f.k[q];
+  }
+  // redirection: A_xy += U~_x^* F_xy V~_y  (P2P) | F V~ (P2L) | U~^* F (M2P)
+  std::vector<std::pair<std::pair<int, int>, double*>> p2p;
+  for (auto& pr : S)
+    for (int dir = 0; dir < 2; ++dir) {
+      int x = dir ? pr.second : pr.first, y = dir ? pr.first : pr.second;
+      const Blk& F = f.F.at(f.key(x, y));
+      if (!f.E[x] && !f.E[y]) {
+        double* tp = c.work.d((size_t)f.m[x] * std::max(f.k[y], 1));
+        g.task(tp, f.m[x], f.m[x], f.k[y], 0.0);
+        g.term(1.0, F.p, F.ld, 0, f.V[y], f.m[y], 0, f.m[y]);
+        p2p.push_back({{x, y}, tp});
+      }
+    }
+  g.run(c.up, c.s, &c.fc_all);
+  size_t pi_ = 0;
+  for (auto& pr : S)
+    for (int dir = 0; dir < 2; ++dir) {
+      int x = dir ? pr.second : pr.first, y = dir ? pr.first : pr.second;
+      const Blk& F = f.F.at(f.key(x, y));
+      const Blk& A = f.A.at(f.key(x, y));
+      if (!f.E[x] && !f.E[y]) {
+        double* tp = p2p[pi_++].second;
+        g.task(A.p, A.ld, f.k[x], f.k[y], 1.0);
+        g.term(1.0, f.U[x], f.m[x], 1, tp, f.m[x], 0, f.m[x]);
+      } else if (f.E[x] && !f.E[y]) {
+        g.task(A.p, A.ld, f.k[x], f.k[y], 1.0);
+        g.term(1.0, F.p, F.ld, 0, f.V[y], f.m[y], 0, f.m[y]);
+      } else {
+        g.task(A.p, A.ld, f.k[x], f.k[y], 1.0);
+        g.term(1.0, f.U[x], f.m[x], 1, F.p, F.ld, 0, f.m[x]);
+      }
+      cb.fill(F.p, F.ld, live(f, x), live(f, y), 0.0);
+    }
+  g.run(c.up, c.s, &c.fc_all);
+  cb.run(c.up, c.s);
+  for (auto& pr : S) f.pending.erase(pr);
+}
+
+static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
+  const int l = f.l;
+  if (g_prof.on) g_prof.begin(c.s);
+  // 1. assemble P_i = [[K_ii, U_i],[V_i^T, 0]] into G_i and invert in place (R16)
+  CopyBatch cb;
+  std::vector<InvReq> inv;
+  int* dinfo = c.work.i(cs.size());
+  for (size_t a = 0; a < cs.size(); ++a) {
+    int i = cs[a];
+    const int m = f.m[i], k = f.k[i], n = m + k;
+    Rec& r = f.rec[i];
+    r.m = m;
+    r.k = k;
+    r.G = c.persist.d(std::max<size_t>((size_t)n * n, 1));
+    if (!n) continue;
+    const Blk& K = f.nearb.at(f.key(i, i));
+    cb.copy(K.p, K.ld, r.G, n, m, m);
+    cb.copy(f.U[i], m, r.G + (size_t)m * n, n, m, k);
+    cb.copy(f.V[i], m, r.G + m, n, k, m, 1.0, 1);
+    cb.fill(r.G + (size_t)m * n + m, n, k, k, 0.0);
+    inv.push_back(InvReq{r.G, n, n, dinfo + a});
+  }
+  cb.run(c.up, c.s);
+  AIFMM_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int) * cs.size(), c.s));
+  batched_inverse(inv, c.work, c.up, c.s, &c.fc_all);
+  if (g_prof.on) { g_prof.end("elim.inverse"); g_prof.begin(c.s); }
+  // 2. W_i = G[:, 0:m] * R_i (row X_i blocks), columns ordered as N(i) \ i
+  std::vector<std::vector<int>> nbs(cs.size());
+  std::vector<double*> W(cs.size());
+  std::vector<std::unordered_map<int, int>> wcol(cs.size());
+  GemmBatch g;
+  for (size_t a = 0; a < cs.size(); ++a) {
+    int i = cs[a];
+    const int m = f.m[i], n = m + f.k[i];
+    int nn_;
+    const int* nl = c.nlist(l, i, &nn_);
+    int tot = 0;
+    for (int t = 0; t < nn_; ++t)
+      if (nl[t] != i) { nbs[a].push_back(nl[t]); wcol[a][nl[t]] = tot; tot += live(f, nl[t]); }
+    W[a] = c.work.d(std::max<size_t>((size_t)n * tot, 1));
+    if (!n) continue;
+    for (int q : nbs[a]) {
+      const Blk& R = f.nearb.at(f.key(i, q));
+      if (!live(f, q)) continue;
+      g.task(W[a] + (size_t)wcol[a][q] * n, n, n, live(f, q), 0.0);
+      g.term(1.0, f.rec[i].G, n, 0, R.p, R.ld, 0, m);
+    }
+  }
+  g.run(c.up, c.s, &c.fc_all);
+  // 3. Schur updates, target-centric (deterministic ascending-i accumulation), + new blocks
+  std::map<std::pair<int, int>, std::vector<int>> targets;   // (p,q) -> list of a (index into cs)
+  for (size_t a = 0; a < cs.size(); ++a)
+    for (int p : nbs[a])
+      for (int q : nbs[a]) targets[{p, q}].push_back((int)a);
+  for (auto& kv : targets) {
+    const int p = kv.first.first, q = kv.first.second;
+    const int M = live(f, p), N = live(f, q);
+    if (!M || !N) continue;
+    Blk T;
+    auto it = f.nearb.find(f.key(p, q));
+    if (it != f.nearb.end()) T = it->second;
+    else if (f.E[p] && f.E[q]) T = f.A.at(f.key(p, q));
+    else {
+      T = f.F.at(f.key(p, q));
+      AIFMM_REQUIRE(c.cheb(l, p, q) == 2, AIFMM_ESINGULAR_PIVOT, "fill-in outside N and IL");
+      f.pending.insert({std::min(p, q), std::max(p, q)});
+    }
+    g.task(T.p, T.ld, M, N, 1.0);
+    for (int a : kv.second) {
+      int i = cs[a];
+      const int m = f.m[i], n = m + f.k[i];
+      if (!m) continue;
+      const Blk& C = f.nearb.at(f.key(p, i));
+      g.term(-1.0, C.p, C.ld, 0, W[a] + (size_t)wcol[a][q] * n, n, 0, m);
+    }
+  }
+  // new blocks (p,i) = C G12, (i,q) = G21 R = W_z, (i,i) = -G22 (R17)
+  std::vector<std::pair<long long, Blk>> fresh;
+  for (size_t a = 0; a < cs.size(); ++a) {
+    int i = cs[a];
+    const int m = f.m[i], k = f.k[i], n = m + k;
+    Rec& r = f.rec[i];
+    for (int p : nbs[a]) {
+      const Blk& C = f.nearb.at(f.key(p, i));
+      r.C.push_back({p, C});
+      r.Ckind_z.push_back(f.E[p]);
+      Blk nb_{c.persist.d(std::max<size_t>((size_t)live(f, p) * k, 1)), std::max(live(f, p), 1), live(f, p), k};
+      if (live(f, p) && k) {
+        g.task(nb_.p, nb_.ld, live(f, p), k, 0.0);
+        if (m) g.term(1.0, C.p, C.ld, 0, r.G + (size_t)m * n, n, 0, m);
+      }
+      fresh.push_back({f.key(p, i), nb_});
+    }
+    for (int q : nbs[a]) {
+      const Blk& R = f.nearb.at(f.key(i, q));
+      r.R.push_back({q, R});
+      r.Rkind_y.push_back(f.E[q]);
+      Blk nb_{c.persist.d(std::max<size_t>((size_t)k * live(f, q), 1)), std::max(k, 1), k, live(f, q)};
+      cb.copy(W[a] + (size_t)wcol[a][q] * n + m, n, nb_.p, nb_.ld, k, live(f, q));
+      fresh.push_back({f.key(i, q), nb_});
+    }
+    Blk nb_{c.persist.d(std::max<size_t>((size_t)k * k, 1)), std::max(k, 1), k, k};
+    cb.copy(r.G + (size_t)m * n + m, n, nb_.p, nb_.ld, k, k, -1.0);
+    fresh.push_back({f.key(i, i), nb_});
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c.timing) {
+    AIFMM_CUDA(cudaEventCreate(&e0));
+    AIFMM_CUDA(cudaEventCreate(&e1));
+    AIFMM_CUDA(cudaEventRecord(e0, c.s));
+  }
+  if (g_prof.on) { g_prof.end("elim.W+plan"); g_prof.begin(c.s); }
+  long long l0 = g_launches;
+  g.run(c.up, c.s, &c.fc_schur);
+  c.stats[AIFMM_STAT_SCHUR_LAUNCHES] += (double)(g_launches - l0);
+  if (c.timing) {
+    AIFMM_CUDA(cudaEventRecord(e1, c.s));
+    c.ev.push_back({e0, e1});
+  }
+  cb.run(c.up, c.s);
+  if (g_prof.on) { g_prof.end("elim.schur"); g_prof.begin(c.s); }
+  for (auto& fr : fresh) f.nearb[fr.first] = fr.second;
+  for (int i : cs) f.E[i] = 1;
+  std::vector<int> info = d2h(c, dinfo, cs.size());
+  for (size_t a = 0; a < cs.size(); ++a)
+    if (info[a])
+      throw Error(AIFMM_ESINGULAR_PIVOT, "singular pivot at level " + std::to_string(l) + " box " + std::to_string(cs[a]));
+  c.work.reset();
+  if (g_prof.on) g_prof.end("elim.tail");
+}
+
+static void factor_all(Ctx& c) {
+  const int L = c.L;
+  c.fl.assign(L + 1, FLevel{});
+  for (int l = L; l >= 2; --l) {
+    g_prof.begin(c.s);
+    setup_level(c, l);
+    check_flag(c, AIFMM_ECOINCIDENT, "coincident points with a singular kernel");
+    FLevel& f = c.fl[l];
+    g_prof.end("setup");
+    g_prof.begin(c.s);
+    orthonormalise(c, f);
+    g_prof.end("orth");
+    int ncol = 0;
+    for (int b : f.boxes) ncol = std::max(ncol, c.col[l][b] + 1);
+    for (int col = 0; col < ncol; ++col) {
+      std::vector<int> cs;
+      for (int b : f.boxes)
+        if (c.col[l][b] == col) cs.push_back(b);
+      std::vector<std::pair<int, int>> S;
+      for (auto& pr : f.pending)
+        if (c.col[l][pr.first] == col || c.col[l][pr.second] == col) S.push_back(pr);
+      g_prof.begin(c.s);
+      if (!S.empty()) compress(c, f, S);
+      g_prof.end("compress");
+      g_prof.begin(c.s);
+      eliminate_colour(c, f, cs);
+      g_prof.end("eliminate");
+    }
+    AIFMM_REQUIRE(f.pending.empty(), AIFMM_ESINGULAR_PIVOT, "pending far fill-ins at level end");
+    for (int b : f.boxes) c.stats[AIFMM_STAT_MAX_RANK] = std::max(c.stats[AIFMM_STAT_MAX_RANK], (double)f.k[b]);
+    // solve layout
+    f.xrow.assign(f.nb + 1, 0);
+    f.zrow.assign(f.nb + 1, 0);
+    for (int b = 0; b < f.nb; ++b) {
+      f.xrow[b + 1] = f.xrow[b] + f.m[b];
+      f.zrow[b + 1] = f.zrow[b] + f.k[b];
+    }
+    f.Xtot = f.xrow[f.nb];
+    f.Ztot = f.zrow[f.nb];
+  }
+  // top: M = (Z_p, y_q) over level-2 boxes; inverted in place (R19 dense GJ)
+  g_prof.begin(c.s);
+  FLevel& f = c.fl[2];
+  c.topn = (int)f.Ztot;
+  c.topoff = f.zrow;
+  c.topinv = c.persist.d(std::max<size_t>((size_t)c.topn * c.topn, 1));
+  CopyBatch cb;
+  for (int p : f.boxes)
+    for (int q : f.boxes) {
+      if (!f.k[p] || !f.k[q]) continue;
+      auto it = f.nearb.find(f.key(p, q));
+      const Blk& B = (it != f.nearb.end()) ? it->second : f.A.at(f.key(p, q));
+      cb.copy(B.p, B.ld, c.topinv + (size_t)f.zrow[q] * c.topn + f.zrow[p], c.topn, f.k[p], f.k[q]);
+    }
+  cb.run(c.up, c.s);
+  if (c.topn) {
+    int* dinfo = c.work.i(1);
+    AIFMM_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int), c.s));
+    batched_inverse(std::vector<InvReq>{InvReq{c.topinv, c.topn, c.topn, dinfo}}, c.work, c.up, c.s, &c.fc_all);
+    int info = d2h(c, dinfo, 1)[0];
+    if (info) throw Error(AIFMM_ESINGULAR_PIVOT, "singular top-level system");
+  }
+  c.stats[AIFMM_STAT_TOP_SIZE] = c.topn;
+  c.work.reset();
+  g_prof.end("top");
+  g_prof.dump("factor");
+}
+
+// ------------------------------------------------------------------------------------ solve
+static void solve_dev(Ctx& c, double* B, int nrhs) {
+  const int L = c.L;
+  const long long n = c.n;
+  DevPool& W = c.work;
+  W.reset();
+  double* Bs = W.d((size_t)n * nrhs);
+  LAUNCH(permute_rows_kernel, gsz(n * nrhs), 256, 0, c.s, B, Bs, c.perm, n, nrhs, 0);
+  std::vector<double*> RZ(L + 2, nullptr), SX(L + 1, nullptr);
+  for (int l = 2; l <= L; ++l) {
+    RZ[l] = W.d(std::max<long long>(c.fl[l].Ztot * nrhs, 1));
+    AIFMM_CUDA(cudaMemsetAsync(RZ[l], 0, sizeof(double) * c.fl[l].Ztot * nrhs, c.s));
+    SX[l] = (l == L) ? W.d((size_t)n * nrhs) : W.d(std::max<long long>(c.fl[l].Xtot * nrhs, 1));
+  }
+  auto RXp = [&](int l, int b, int* ld) -> double* {
+    if (l == L) { *ld = (int)n; return Bs + c.off[L][b]; }
+    *ld = (int)c.fl[l + 1].Ztot;
+    return RZ[l + 1] + c.fl[l].xrow[b];
+  };
+  // forward (Alg. 4 replays the eliminations on the rhs; T_As includes it)
+  for (int l = L; l >= 2; --l) {
+    FLevel& f = c.fl[l];
+    int ncol = 0;
+    for (int b : f.boxes) ncol = std::max(ncol, c.col[l][b] + 1);
+    const int ldz = (int)f.Ztot;
+    for (int col = 0; col < ncol; ++col) {
+      std::vector<int> cs;
+      for (int b : f.boxes)
+        if (c.col[l][b] == col) cs.push_back(b);
+      GemmBatch g;
+      std::vector<double*> w(cs.size());
+      for (size_t a = 0; a < cs.size(); ++a) {
+        const Rec& r = f.rec[cs[a]];
+        const int nn = r.m + r.k;
+        w[a] = W.d(std::max<size_t>((size_t)nn * nrhs, 1));
+        if (!nn || !r.m) {
+          if (nn) { CopyBatch z; z.fill(w[a], nn, nn, nrhs, 0.0); z.run(c.up, c.s); }
+          continue;
+        }
+        int ld;
+        double* rx = RXp(l, cs[a], &ld);
+        g.task(w[a], nn, nn, nrhs, 0.0);
+        g.term(1.0, r.G, nn, 0, rx, ld, 0, r.m);
+      }
+      g.run(c.up, c.s, &c.fc_all);
+      // targets: (p, row-kind) -> contributions
+      std::map<std::pair<int, int>, std::vector<std::pair<int, int>>> tg;   // -> (a, idx in C)
+      for (size_t a = 0; a < cs.size(); ++a) {
+        const Rec& r = f.rec[cs[a]];
+        for (size_t t = 0; t < r.C.size(); ++t) tg[{r.C[t].first, (int)r.Ckind_z[t]}].push_back({(int)a, (int)t});
+        tg[{cs[a], 2}].push_back({(int)a, -1});
+      }
+      for (auto& kv : tg) {
+        const int p = kv.first.first, kind = kv.first.second;
+        double* C;
+        int ldc, M;
+        if (kind == 0) { C = RXp(l, p, &ldc); M = f.m[p]; }
+        else { C = RZ[l] + f.zrow[p]; ldc = ldz; M = f.k[p]; }
+        if (!M) continue;
+        g.task(C, ldc, M, nrhs, 1.0);
+        for (auto& at : kv.second) {
+          const Rec& r = f.rec[cs[at.first]];
+          const int nn = r.m + r.k;
+          if (at.second < 0) {
+            if (r.k) g.add(1.0, w[at.first] + r.m, nn, 0);
+          } else {
+            const Blk& Cb = r.C[at.second].second;
+            if (r.m) g.term(-1.0, Cb.p, Cb.ld, 0, w[at.first], nn, 0, r.m);
+          }
+        }
+      }
+      g.run(c.up, c.s, &c.fc_all);
+    }
+  }
+  // top: y2 = M^{-1} b_Z
+  double* y2 = W.d(std::max<long long>((long long)c.topn * nrhs, 1));
+  {
+    GemmBatch g;
+    if (c.topn) {
+      g.task(y2, c.topn, c.topn, nrhs, 0.0);
+      g.term(1.0, c.topinv, c.topn, 0, RZ[2], c.topn, 0, c.topn);
+    }
+    g.run(c.up, c.s, &c.fc_all);
+  }
+  // backward
+  for (int l = 2; l <= L; ++l) {
+    FLevel& f = c.fl[l];
+    double* Y = (l == 2) ? y2 : SX[l - 1];
+    const int ldy = (int)f.Ztot;
+    double* X = SX[l];
+    const int ldx = (l == L) ? (int)n : (int)f.Xtot;
+    auto xrow = [&](int b) -> long long { return (l == L) ? c.off[L][b] : f.xrow[b]; };
+    int ncol = 0;
+    for (int b : f.boxes) ncol = std::max(ncol, c.col[l][b] + 1);
+    for (int col = ncol - 1; col >= 0; --col) {
+      std::vector<int> cs;
+      for (int b : f.boxes)
+        if (c.col[l][b] == col) cs.push_back(b);
+      CopyBatch cb;
+      GemmBatch g;
+      std::vector<double*> tmp(cs.size());
+      for (size_t a = 0; a < cs.size(); ++a) {
+        const int i = cs[a];
+        const Rec& r = f.rec[i];
+        const int nn = r.m + r.k;
+        tmp[a] = W.d(std::max<size_t>((size_t)nn * nrhs, 1));
+        int ld;
+        double* rx = RXp(l, i, &ld);
+        cb.copy(rx, ld, tmp[a], nn, r.m, nrhs);
+        cb.copy(Y + f.zrow[i], ldy, tmp[a] + r.m, nn, r.k, nrhs);
+      }
+      cb.run(c.up, c.s);
+      for (size_t a = 0; a < cs.size(); ++a) {
+        const int i = cs[a];
+        const Rec& r = f.rec[i];
+        const int nn = r.m + r.k;
+        if (!r.m) continue;
+        g.task(tmp[a], nn, r.m, nrhs, 1.0);
+        for (size_t t = 0; t < r.R.size(); ++t) {
+          const int q = r.R[t].first;
+          const Blk& Rb = r.R[t].second;
+          if (r.Rkind_y[t]) {
+            if (f.k[q]) g.term(-1.0, Rb.p, Rb.ld, 0, Y + f.zrow[q], ldy, 0, f.k[q]);
+          } else {
+            if (f.m[q]) g.term(-1.0, Rb.p, Rb.ld, 0, X + xrow(q), ldx, 0, f.m[q]);
+          }
+        }
+      }
+      g.run(c.up, c.s, &c.fc_all);
+      for (size_t a = 0; a < cs.size(); ++a) {
+        const int i = cs[a];
+        const Rec& r = f.rec[i];
+        const int nn = r.m + r.k;
+        if (!r.m) continue;
+        g.task(X + xrow(i), ldx, r.m, nrhs, 0.0);
+        g.term(1.0, r.G, nn, 0, tmp[a], nn, 0, nn);
+      }
+      g.run(c.up, c.s, &c.fc_all);
+    }
+  }
+  LAUNCH(permute_rows_kernel, gsz(n * nrhs), 256, 0, c.s, SX[L], B, c.perm, n, nrhs, 1);
+  c.up.sync();
+  W.reset();
+}
+
+}  // namespace aifmm
+
+// ====================================================================================== C-ABI
+using namespace aifmm;
+
+#define CAPI_BEGIN try {
+#define CAPI_END                                      \
+  }                                                   \
+  catch (const aifmm::Error& e) {                     \
+    g_err = e.what();                                 \
+    return e.code;                                    \
+  }                                                   \
+  catch (const std::exception& e) {                   \
+    g_err = e.what();                                 \
+    return AIFMM_ECUDA;                               \
+  }                                                   \
+  g_err.clear();                                      \
+  return AIFMM_OK;
+
+static double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+extern "C" {
+
+int aifmm_build(const double* points, int64_t n, int d, int kernel_id, const double* kparams, int leaf_size,
+                double tol) {
+  CAPI_BEGIN
+  AIFMM_REQUIRE(points && kparams, AIFMM_EINVALID_ARG, "null pointer");
+  AIFMM_REQUIRE(n >= 1 && n < (1ll << 31), AIFMM_EINVALID_ARG, "n out of range");
+  AIFMM_REQUIRE(d == 2 || d == 3, AIFMM_EINVALID_ARG, "d must be 2 or 3");
+  AIFMM_REQUIRE(kernel_id >= 0 && kernel_id <= 2, AIFMM_EINVALID_ARG, "unknown kernel id");
+  AIFMM_REQUIRE(leaf_size >= 1 && leaf_size <= 4096, AIFMM_EINVALID_ARG, "leaf_size out of range");
+  AIFMM_REQUIRE(tol > 0.0 && tol < 1.0, AIFMM_EINVALID_ARG, "tol must lie in (0,1)");
+  Ctx& c = ctx();
+  auto t0 = std::chrono::steady_clock::now();
+  c.persist.release();
+  c.buildp.release();
+  c.work.reset();
+  c.fl.clear();
+  c.nn.clear();
+  c.built = c.factored = false;
+  c.n = n;
+  c.d = d;
+  c.kid = kernel_id;
+  c.leaf = leaf_size;
+  c.tol = tol;
+  c.kp = KernelParams{kernel_id, d, kparams[0], kparams[1]};
+  if (kernel_id == 1) AIFMM_REQUIRE(kparams[1] > 0.0, AIFMM_EINVALID_ARG, "ell must be > 0");
+  g_prof.on = getenv("AIFMM_PROFILE") != nullptr;
+  g_prof.begin(c.s);
+  build_tree(c, points);
+  g_prof.end("tree");
+  g_prof.begin(c.s);
+  build_nnca(c);
+  g_prof.end("nnca");
+  g_prof.dump("build");
+  c.buildp.release();
+  c.built = true;
+  c.stats[AIFMM_STAT_LEVELS] = c.L;
+  c.stats[AIFMM_STAT_BUILD_MS] = ms_since(t0);
+  CAPI_END
+}
+
+int aifmm_set_compression_tol(double tol_c) {
+  CAPI_BEGIN
+  AIFMM_REQUIRE(tol_c >= 0.0 && tol_c < 1.0, AIFMM_EINVALID_ARG, "tol_c must lie in [0,1)");
+  ctx().tol_c_user = tol_c;
+  CAPI_END
+}
+
+int aifmm_factor(void) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built, AIFMM_ESTATE, "factor before build");
+  auto t0 = std::chrono::steady_clock::now();
+  if (c.factored) {
+    // re-factor from the same build: drop the previous factor storage but keep NNCA
+    throw Error(AIFMM_ESTATE, "already factored: call aifmm_build again");
+  }
+  c.tol_c = (c.tol_c_user >= 0) ? c.tol_c_user : c.tol;
+  for (auto& e : c.ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  c.ev.clear();
+  factor_all(c);
+  c.up.sync();
+  double sch = 0.0;
+  for (auto& e : c.ev) {
+    float ms = 0.f;
+    AIFMM_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+    sch += ms;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c.ev.clear();
+  c.stats[AIFMM_STAT_SCHUR_MS] += sch;
+  c.stats[AIFMM_STAT_SCHUR_FLOPS] = c.fc_schur.flops;
+  c.stats[AIFMM_STAT_SCHUR_BYTES] = c.fc_schur.bytes;
+  c.stats[AIFMM_STAT_FACTOR_FLOPS] = c.fc_all.flops + c.fc_schur.flops;
+  c.factored = true;
+  c.stats[AIFMM_STAT_FACTOR_MS] = ms_since(t0);
+  c.stats[AIFMM_STAT_DEVICE_BYTES] = (double)c.persist.total();
+  CAPI_END
+}
+
+int aifmm_solve(double* B, int nrhs) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.factored, AIFMM_ESTATE, "solve before factor");
+  AIFMM_REQUIRE(B && nrhs >= 1, AIFMM_EINVALID_ARG, "bad right-hand side");
+  auto t0 = std::chrono::steady_clock::now();
+  AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
+  LAUNCH(finite_kernel, gsz(c.n * nrhs), 256, 0, c.s, B, c.n * nrhs, c.dflag);
+  check_flag(c, AIFMM_ENONFINITE, "non-finite right-hand side");
+  solve_dev(c, B, nrhs);
+  c.stats[AIFMM_STAT_SOLVE_MS] = ms_since(t0);
+  CAPI_END
+}
+
+int aifmm_solve_host(double* B, int nrhs) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.factored, AIFMM_ESTATE, "solve before factor");
+  AIFMM_REQUIRE(B && nrhs >= 1, AIFMM_EINVALID_ARG, "bad right-hand side");
+  double* dB = nullptr;
+  size_t bytes = sizeof(double) * c.n * nrhs;
+  AIFMM_CUDA(cudaMalloc(&dB, bytes));
+  try {
+    AIFMM_CUDA(cudaMemcpyAsync(dB, B, bytes, cudaMemcpyHostToDevice, c.s));
+    int rc = aifmm_solve(dB, nrhs);
+    if (rc) throw Error(rc, g_err);
+    AIFMM_CUDA(cudaMemcpyAsync(B, dB, bytes, cudaMemcpyDeviceToHost, c.s));
+    AIFMM_CUDA(cudaStreamSynchronize(c.s));
+  } catch (...) {
+    cudaFree(dB);
+    throw;
+  }
+  cudaFree(dB);
+  CAPI_END
+}
+
+void aifmm_free(void) {
+  if (!g_ctx) return;
+  Ctx& c = *g_ctx;
+  if (c.s) cudaStreamSynchronize(c.s);
+  c.fl.clear();
+  c.nn.clear();
+  c.persist.release();
+  c.work.release();
+  c.buildp.release();
+  c.built = c.factored = false;
+  c.tol_c_user = -1;
+}
+
+const char* aifmm_last_error(void) { return g_err.c_str(); }
+
+int aifmm_set_stream(void* stream) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_CUDA(cudaStreamSynchronize(c.s));
+  if (c.own_stream) cudaStreamDestroy(c.s);
+  c.s = static_cast<cudaStream_t>(stream);
+  c.own_stream = false;
+  c.up.free_all();
+  c.up.init(c.s);
+  CAPI_END
+}
+
+int aifmm_get_tree(int64_t* perm, int* L) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built, AIFMM_ESTATE, "no build");
+  if (L) *L = c.L;
+  if (perm) {
+    std::vector<int> p = d2h(c, c.perm, c.n);
+    for (long long i = 0; i < c.n; ++i) perm[i] = p[i];
+  }
+  CAPI_END
+}
+
+int aifmm_get_level_offsets(int level, int64_t* off) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built && level >= 0 && level <= c.L && off, AIFMM_EINVALID_ARG, "bad level");
+  for (size_t i = 0; i < c.off[level].size(); ++i) off[i] = c.off[level][i];
+  CAPI_END
+}
+
+int aifmm_get_lists(int level, int32_t* n_ptr, int32_t* n_idx, int32_t* il_ptr, int32_t* il_idx) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built && level >= 2 && level <= c.L && n_ptr && il_ptr, AIFMM_EINVALID_ARG, "bad level");
+  const int nb = 1 << (c.d * level);
+  n_ptr[0] = il_ptr[0] = 0;
+  for (int b = 0; b < nb; ++b) {
+    n_ptr[b + 1] = n_ptr[b] + c.ncnt[level][b];
+    il_ptr[b + 1] = il_ptr[b] + c.icnt[level][b];
+    if (n_idx)
+      for (int t = 0; t < c.ncnt[level][b]; ++t) n_idx[n_ptr[b] + t] = c.nidx[level][(size_t)b * c.ncap + t];
+    if (il_idx)
+      for (int t = 0; t < c.icnt[level][b]; ++t) il_idx[il_ptr[b] + t] = c.iidx[level][(size_t)b * c.icap + t];
+  }
+  CAPI_END
+}
+
+int aifmm_get_colours(int level, int32_t* colour) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built && level >= 2 && level <= c.L && colour, AIFMM_EINVALID_ARG, "bad level");
+  for (size_t b = 0; b < c.col[level].size(); ++b) colour[b] = c.col[level][b];
+  CAPI_END
+}
+
+int aifmm_get_ranks(int level, int which, int32_t* ranks) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built && level >= 2 && level <= c.L && ranks, AIFMM_EINVALID_ARG, "bad level");
+  const int nb = 1 << (c.d * level);
+  for (int b = 0; b < nb; ++b) {
+    if (which == 0) ranks[b] = c.nn[level].k[b];
+    else {
+      AIFMM_REQUIRE(c.factored, AIFMM_ESTATE, "not factored");
+      ranks[b] = c.fl[level].k[b];
+    }
+  }
+  CAPI_END
+}
+
+int aifmm_stats(double* out) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  c.stats[AIFMM_STAT_LAUNCHES] = (double)g_launches;
+  c.stats[AIFMM_STAT_HOST_SYNCS] = (double)c.up.syncs;
+  for (int i = 0; i < AIFMM_NSTATS; ++i) out[i] = c.stats[i];
+  CAPI_END
+}
+
+int aifmm_reset_counters(void) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  g_launches = 0;
+  c.up.syncs = 0;
+  c.fc_all = FlopCounter{};
+  c.fc_schur = FlopCounter{};
+  c.stats[AIFMM_STAT_SCHUR_MS] = 0;
+  c.stats[AIFMM_STAT_SCHUR_LAUNCHES] = 0;
+  c.stats[AIFMM_STAT_COMPRESSIONS] = 0;
+  c.stats[AIFMM_STAT_MAX_RANK] = 0;
+  CAPI_END
+}
+
+int aifmm_debug_inverse(double* A, int n, int lda) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  int* dinfo = c.work.i(1);
+  AIFMM_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int), c.s));
+  batched_inverse(std::vector<InvReq>{InvReq{A, lda, n, dinfo}}, c.work, c.up, c.s);
+  int info = d2h(c, dinfo, 1)[0];
+  c.work.reset();
+  if (info) throw Error(AIFMM_ESINGULAR_PIVOT, "singular matrix");
+  CAPI_END
+}
+
+int aifmm_set_timing(int on) {
+  CAPI_BEGIN
+  ctx().timing = on != 0;
+  CAPI_END
+}
+
+}  // extern "C"

@@ -1,0 +1,620 @@
+// dense_kernels.cu — batched variable-size dense FP64 kernels of the AIFMM hot path (sm_100a).
+//
+//   gemm_tasks_kernel  : C = beta C + sum_t alpha_t op(A_t) op(B_t) on FP64 tensor cores
+//                        (mma.sync m8n8k4 f64 -> SASS DMMA; tcgen05 has no f64 kind on sm_100a).
+//                        Used for the Schur-complement updates (Table 4),
+//                        the multipliers W = P_i^{-1} R_i, projections / redirections
+//                         and the solve (Alg. 4).
+//   gj_tasks_kernel    : Gauss-Jordan with partial pivoting (pivot inverse G = P_i^{-1}, the
+//                        NNCA skeleton solve A(fp,sk)^{-1} A(fp,R) of P:361/P:365, top solve).
+//   pqr_tasks_kernel   : column-pivoted Gram-Schmidt with truncation (the paper's RRQR).
+//   keval_tasks_kernel : kernel-entry blocks A(rows, cols).
+//   copy/norm kernels  : block assembly, level transition gathers, Frobenius norms.
+#include "common.cuh"
+
+namespace aifmm {
+
+// ------------------------------------------------------------------------------ DMMA GEMM
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int BM, int BN>
+__global__ void __launch_bounds__(BM * BN / 32)
+gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmTerm* __restrict__ terms,
+                  const GemmTile* __restrict__ tiles) {
+  constexpr int BK = 16;
+  constexpr int NT = BM * BN / 32;           // threads (one warp per 32x32 sub-tile)
+  constexpr int LDS_A = BM + 4;              // (BM+4) % 16 == 4 -> conflict-free fragment loads
+  constexpr int LDS_B = BN + 4;
+  __shared__ double sA[BK][LDS_A];
+  __shared__ double sB[BK][LDS_B];
+
+  const GemmTile tile = tiles[blockIdx.x];
+  const GemmTask tk = tasks[tile.task];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int WARPS_M = BM / 32;
+  const int wm = (warp % WARPS_M) * 32, wn = (warp / WARPS_M) * 32;
+  const int m0 = tile.m0, n0 = tile.n0;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int t = tk.term_begin; t < tk.term_end; ++t) {
+    const GemmTerm tm = terms[t];
+    if (tm.A == nullptr) continue;  // additions are applied in the epilogue
+    const double alpha = tm.alpha;
+    for (int k0 = 0; k0 < tm.K; k0 += BK) {
+      // A tile: op(A)[m0:m0+BM, k0:k0+BK] -> sA[k][m]
+      for (int e = tid; e < BM * BK; e += NT) {
+        int mm, kk;
+        if (!tm.transA) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
+        int gm = m0 + mm, gk = k0 + kk;
+        double v = 0.0;
+        if (gm < tk.M && gk < tm.K)
+          v = tm.transA ? tm.A[(size_t)gm * tm.lda + gk] : tm.A[(size_t)gk * tm.lda + gm];
+        sA[kk][mm] = alpha * v;
+      }
+      // B tile: op(B)[k0:k0+BK, n0:n0+BN] -> sB[k][n]
+      for (int e = tid; e < BN * BK; e += NT) {
+        int nn, kk;
+        if (!tm.transB) { kk = e % BK; nn = e / BK; } else { nn = e % BN; kk = e / BN; }
+        int gn = n0 + nn, gk = k0 + kk;
+        double v = 0.0;
+        if (gn < tk.N && gk < tm.K)
+          v = tm.transB ? tm.B[(size_t)gk * tm.ldb + gn] : tm.B[(size_t)gn * tm.ldb + gk];
+        sB[kk][nn] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = sA[kk + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = sB[kk + (lane & 3)][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+      __syncthreads();
+    }
+  }
+  // epilogue: C = beta*C + acc + sum(addition terms)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + wm + i * 8 + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gn = n0 + wn + j * 8 + (lane & 3) * 2 + e;
+        if (gm < tk.M && gn < tk.N) {
+          double v = acc[i][j][e];
+          for (int t = tk.term_begin; t < tk.term_end; ++t) {
+            const GemmTerm tm = terms[t];
+            if (tm.A != nullptr) continue;
+            v += tm.alpha * (tm.transB ? tm.B[(size_t)gm * tm.ldb + gn] : tm.B[(size_t)gn * tm.ldb + gm]);
+          }
+          double* c = tk.C + (size_t)gn * tk.ldc + gm;
+          *c = (tk.beta == 0.0) ? v : tk.beta * (*c) + v;
+        }
+      }
+    }
+  }
+}
+
+template __global__ void gemm_tasks_kernel<64, 64>(const GemmTask*, const GemmTerm*, const GemmTile*);
+template __global__ void gemm_tasks_kernel<32, 32>(const GemmTask*, const GemmTerm*, const GemmTile*);
+template __global__ void gemm_tasks_kernel<64, 32>(const GemmTask*, const GemmTerm*, const GemmTile*);
+template __global__ void gemm_tasks_kernel<32, 64>(const GemmTask*, const GemmTerm*, const GemmTile*);
+
+// ------------------------------------------------------------------------------ block reductions
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (lane < NT / 32) ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+template <int NT>
+__device__ __forceinline__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (lane < NT / 32) ? red[lane] : -1.0;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+template <int NT>
+__device__ __forceinline__ int block_min_int(int v, int* red) {
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (lane < NT / 32) ? red[lane] : 0x7fffffff;
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  int r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------------------ Gauss-Jordan
+// Unblocked Gauss-Jordan with partial pivoting on an n x ncols column-major matrix M (ld).
+// mode 0: [A | B] -> [I | A^{-1} B];  mode 1: in-place inverse of A (n x n).
+// Returns the failing step + 1 (exact zero pivot) or 0.
+constexpr int GJ_NT = 256;
+__device__ int gj_device(double* M, int ld, int n, int nc, int mode, double* f, int* piv, double* red, int* redi) {
+  const int tid = threadIdx.x;
+  for (int k = 0; k < n; ++k) {
+    double v = -1.0;
+    for (int i = k + tid; i < n; i += GJ_NT) v = fmax(v, fabs(M[(size_t)k * ld + i]));
+    const double mx = block_max<GJ_NT>(v, red);
+    int cand = 0x7fffffff;
+    for (int i = k + tid; i < n; i += GJ_NT)
+      if (fabs(M[(size_t)k * ld + i]) == mx) { cand = i; break; }
+    const int p = block_min_int<GJ_NT>(cand, redi);
+    if (!(mx > 0.0)) return k + 1;
+    if (tid == 0) piv[k] = p;
+    const int jlo = (mode == 1) ? 0 : k;
+    const int jhi = (mode == 1) ? n : nc;
+    if (p != k)
+      for (int j = jlo + tid; j < jhi; j += GJ_NT) {
+        double a = M[(size_t)j * ld + k], b = M[(size_t)j * ld + p];
+        M[(size_t)j * ld + k] = b;
+        M[(size_t)j * ld + p] = a;
+      }
+    __syncthreads();
+    const double d = 1.0 / M[(size_t)k * ld + k];
+    for (int i = tid; i < n; i += GJ_NT) f[i] = M[(size_t)k * ld + i];
+    __syncthreads();
+    for (int j = jlo + tid; j < jhi; j += GJ_NT) {
+      if (j == k) M[(size_t)j * ld + k] = (mode == 1) ? d : 1.0;
+      else M[(size_t)j * ld + k] *= d;
+    }
+    __syncthreads();
+    const int ncol = jhi - jlo;
+    const int tot = ncol * n;
+    for (int e = tid; e < tot; e += GJ_NT) {
+      const int i = e % n, j = jlo + e / n;
+      if (i == k) continue;
+      const double fi = f[i];
+      if (j == k) M[(size_t)j * ld + i] = (mode == 1) ? -fi * d : 0.0;
+      else M[(size_t)j * ld + i] -= fi * M[(size_t)j * ld + k];
+    }
+    __syncthreads();
+  }
+  if (mode == 1) {
+    for (int k = n - 1; k >= 0; --k) {
+      const int p = piv[k];
+      if (p != k)
+        for (int i = tid; i < n; i += GJ_NT) {
+          double a = M[(size_t)k * ld + i], b = M[(size_t)p * ld + i];
+          M[(size_t)k * ld + i] = b;
+          M[(size_t)p * ld + i] = a;
+        }
+      __syncthreads();
+    }
+  }
+  return 0;
+}
+
+// small matrices: staged in shared memory (fast); smem = n*ncols + n doubles + n ints
+__global__ void __launch_bounds__(GJ_NT) gj_small_kernel(const GJTask* __restrict__ tasks, int mode) {
+  extern __shared__ double gsm[];
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  const GJTask tk = tasks[blockIdx.x];
+  const int n = tk.n, nc = (mode == 1) ? n : tk.ncols;
+  if (n == 0) { if (threadIdx.x == 0 && tk.info) *tk.info = 0; return; }
+  double* M = gsm;
+  double* f = M + (size_t)n * nc;
+  int* piv = reinterpret_cast<int*>(f + n);
+  for (int e = threadIdx.x; e < n * nc; e += GJ_NT) M[e] = tk.A[(size_t)(e / n) * tk.lda + (e % n)];
+  __syncthreads();
+  const int info = gj_device(M, n, n, nc, mode, f, piv, red, redi);
+  if (info) { if (threadIdx.x == 0 && tk.info) *tk.info = info; return; }
+  for (int e = threadIdx.x; e < n * nc; e += GJ_NT) tk.A[(size_t)(e / n) * tk.lda + (e % n)] = M[e];
+  if (threadIdx.x == 0 && tk.info) *tk.info = 0;
+}
+
+// large augmented solves in global memory (NNCA skeleton solves that do not fit in smem)
+__global__ void __launch_bounds__(GJ_NT) gj_global_kernel(const GJTask* __restrict__ tasks, int mode) {
+  extern __shared__ double gsm[];
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  const GJTask tk = tasks[blockIdx.x];
+  const int n = tk.n;
+  double* f = gsm;
+  int* piv = reinterpret_cast<int*>(f + n);
+  const int info = gj_device(tk.A, tk.lda, n, (mode == 1) ? n : tk.ncols, mode, f, piv, red, redi);
+  if (threadIdx.x == 0 && tk.info) *tk.info = info;
+}
+
+// ---- blocked in-place Gauss-Jordan inverse for larger matrices (pivot inverses at upper
+// levels, the top system).  Per panel J = [j, j+nbw): panel LU with partial pivoting picks
+// the pivots (identical to GJ's), rows are swapped, D = A[J,J] is inverted from its LU,
+// A[J,:] <- D^{-1} A[J,:], A[R,J] <- 0, B = old A[R,J]; then a DMMA GEMM does A[R,:] -= B A[J,:].
+constexpr int GJB = 32;
+struct GJBTask {
+  double* A;
+  int lda, n;
+  double* PW;    // workspace n x GJB
+  double* Bws;   // workspace n x GJB (ld n)
+  int* piv;      // n
+  int* info;
+};
+
+__global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restrict__ tasks, int j) {
+  const GJBTask tk = tasks[blockIdx.x];
+  const int n = tk.n;
+  if (j >= n) return;
+  if (*tk.info) return;
+  const int nbw = min(GJB, n - j), rows = n - j, ld = tk.lda;
+  double* A = tk.A;
+  double* PW = tk.PW;
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  __shared__ double Li[GJB][GJB + 1], Ui[GJB][GJB + 1], Di[GJB][GJB + 1];
+  __shared__ double ycol[GJ_NT / 32][GJB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < rows * nbw; e += GJ_NT) {
+    const int r = e % rows, c = e / rows;
+    PW[(size_t)c * rows + r] = A[(size_t)(j + c) * ld + j + r];
+  }
+  __syncthreads();
+  for (int c = 0; c < nbw; ++c) {
+    double v = -1.0;
+    for (int r = c + tid; r < rows; r += GJ_NT) v = fmax(v, fabs(PW[(size_t)c * rows + r]));
+    const double mx = block_max<GJ_NT>(v, red);
+    int cand = 0x7fffffff;
+    for (int r = c + tid; r < rows; r += GJ_NT)
+      if (fabs(PW[(size_t)c * rows + r]) == mx) { cand = r; break; }
+    const int p = block_min_int<GJ_NT>(cand, redi);
+    if (!(mx > 0.0)) {
+      if (tid == 0) *tk.info = j + c + 1;
+      return;
+    }
+    if (tid == 0) tk.piv[j + c] = j + p;
+    if (p != c)
+      for (int cc = tid; cc < nbw; cc += GJ_NT) {
+        double a = PW[(size_t)cc * rows + c], b = PW[(size_t)cc * rows + p];
+        PW[(size_t)cc * rows + c] = b;
+        PW[(size_t)cc * rows + p] = a;
+      }
+    __syncthreads();
+    const double dinv = 1.0 / PW[(size_t)c * rows + c];
+    for (int r = c + 1 + tid; r < rows; r += GJ_NT) PW[(size_t)c * rows + r] *= dinv;
+    __syncthreads();
+    const int rem = rows - c - 1, cw = nbw - c - 1;
+    for (int e = tid; e < rem * cw; e += GJ_NT) {
+      const int r = c + 1 + e % rem, cc = c + 1 + e / rem;
+      PW[(size_t)cc * rows + r] -= PW[(size_t)c * rows + r] * PW[(size_t)cc * rows + c];
+    }
+    __syncthreads();
+  }
+  // apply the row interchanges to the full rows of A (in order)
+  for (int c = 0; c < nbw; ++c) {
+    const int p = tk.piv[j + c];
+    if (p != j + c)
+      for (int col = tid; col < n; col += GJ_NT) {
+        double a = A[(size_t)col * ld + j + c], b = A[(size_t)col * ld + p];
+        A[(size_t)col * ld + j + c] = b;
+        A[(size_t)col * ld + p] = a;
+      }
+    __syncthreads();
+  }
+  // D^{-1} = U11^{-1} L11^{-1} from the panel LU (unit lower L11, upper U11)
+  for (int e = tid; e < GJB * GJB; e += GJ_NT) {
+    const int r = e % GJB, c = e / GJB;
+    Li[r][c] = 0.0;
+    Ui[r][c] = 0.0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // column `lane` of L^{-1}: forward substitution
+    if (lane < nbw) {
+      for (int r = 0; r < nbw; ++r) {
+        double s = (r == lane) ? 1.0 : 0.0;
+        for (int t = lane; t < r; ++t) s -= PW[(size_t)t * rows + r] * Li[t][lane];
+        Li[r][lane] = (r < lane) ? 0.0 : s;
+      }
+    }
+  } else if (warp == 1) {
+    // column `lane` of U^{-1}: back substitution
+    if (lane < nbw) {
+      for (int r = nbw - 1; r >= 0; --r) {
+        double s = (r == lane) ? 1.0 : 0.0;
+        for (int t = r + 1; t <= lane; ++t) s -= PW[(size_t)t * rows + r] * Ui[t][lane];
+        Ui[r][lane] = (r > lane) ? 0.0 : s / PW[(size_t)r * rows + r];
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nbw * nbw; e += GJ_NT) {
+    const int r = e % nbw, c = e / nbw;
+    double s = 0.0;
+    for (int t = 0; t < nbw; ++t) s += Ui[r][t] * Li[t][c];
+    Di[r][c] = s;
+  }
+  __syncthreads();
+  // B = A[:, J] with rows J zeroed, A[R, J] = 0, A[J, J] = D^{-1}
+  for (int e = tid; e < n * nbw; e += GJ_NT) {
+    const int r = e % n, c = e / n;
+    const bool inJ = (r >= j && r < j + nbw);
+    tk.Bws[(size_t)c * n + r] = inJ ? 0.0 : A[(size_t)(j + c) * ld + r];
+    A[(size_t)(j + c) * ld + r] = inJ ? Di[r - j][c] : 0.0;
+  }
+  // A[J, c] <- D^{-1} A[J, c] for columns outside J
+  for (int col = warp; col < n; col += GJ_NT / 32) {
+    if (col >= j && col < j + nbw) continue;
+    if (lane < nbw) ycol[warp][lane] = A[(size_t)col * ld + j + lane];
+    __syncwarp();
+    if (lane < nbw) {
+      double s = 0.0;
+      for (int t = 0; t < nbw; ++t) s += Di[lane][t] * ycol[warp][t];
+      A[(size_t)col * ld + j + lane] = s;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void gj_unscramble_kernel(const GJBTask* __restrict__ tasks) {
+  const GJBTask tk = tasks[blockIdx.x];
+  if (*tk.info) return;
+  for (int k = tk.n - 1; k >= 0; --k) {
+    const int p = tk.piv[k];
+    if (p != k)
+      for (int i = threadIdx.x; i < tk.n; i += blockDim.x) {
+        double a = tk.A[(size_t)k * tk.lda + i], b = tk.A[(size_t)p * tk.lda + i];
+        tk.A[(size_t)k * tk.lda + i] = b;
+        tk.A[(size_t)p * tk.lda + i] = a;
+      }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------ pivoted QR
+constexpr int PQR_NT = 256;
+constexpr double TIE = 1e-10;  // reading R7 (same rule as oracle/linalg.py: pick)
+
+__global__ void __launch_bounds__(PQR_NT) pqr_tasks_kernel(const PqrTask* __restrict__ tasks) {
+  extern __shared__ double pq_smem[];
+  const PqrTask tk = tasks[blockIdx.x];
+  const int m = tk.m, nc = tk.ncols, ldw = tk.ldw, ldq = tk.ldq;
+  double* norms = pq_smem;          // nc
+  double* w = norms + nc;           // m
+  double* coef = w + m;             // k0 + tmax
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = PQR_NT / 32;
+  const double tau = tk.tol * (tk.fnorm ? *tk.fnorm : 1.0);
+  double* W = tk.W;
+  double* Q = tk.Q;
+
+  for (int c = warp; c < nc; c += NW) {
+    double s = 0.0;
+    for (int r = lane; r < m; r += 32) { double x = W[(size_t)c * ldw + r]; s += x * x; }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) norms[c] = s;
+  }
+  __syncthreads();
+  int t = 0, t_trunc = -1;
+  while (true) {
+    double part = 0.0;
+    for (int c = tid; c < nc; c += PQR_NT) part += norms[c];
+    const double res2 = block_sum<PQR_NT>(part, red);
+    const bool ok = !(sqrt(res2) > tau);
+    if (ok && t_trunc < 0) t_trunc = t;
+    if (t >= tk.tmin && ok) break;
+    if (t >= tk.tmax) break;
+    double v = -1.0;
+    for (int c = tid; c < nc; c += PQR_NT) v = fmax(v, sqrt(norms[c]));
+    const double mx = block_max<PQR_NT>(v, red);
+    if (!(mx > 0.0)) break;
+    const double thr = mx * (1.0 - TIE);
+    int cand = 0x7fffffff;
+    for (int c = tid; c < nc; c += PQR_NT)
+      if (sqrt(norms[c]) >= thr) { cand = c; break; }
+    const int j = block_min_int<PQR_NT>(cand, redi);
+    for (int r = tid; r < m; r += PQR_NT) w[r] = W[(size_t)j * ldw + r];
+    __syncthreads();
+    const int kb = tk.k0 + t;
+    // re-orthogonalisation (R8): two passes, a third if the second cancelled more than
+    // half; a column still collapsing lies in span(Q) numerically and is discarded
+    double nprev = 0.0, nw = 0.0;
+    for (int pass = 0; pass < 3; ++pass) {
+      for (int s = warp; s < kb; s += NW) {
+        double a = 0.0;
+        for (int r = lane; r < m; r += 32) a += Q[(size_t)s * ldq + r] * w[r];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0) coef[s] = a;
+      }
+      __syncthreads();
+      double p2 = 0.0;
+      for (int r = tid; r < m; r += PQR_NT) {
+        double a = w[r];
+        for (int s = 0; s < kb; ++s) a -= Q[(size_t)s * ldq + r] * coef[s];
+        w[r] = a;
+        p2 += a * a;
+      }
+      nw = sqrt(block_sum<PQR_NT>(p2, red));
+      if (pass == 1 && nw > 0.5 * nprev) break;
+      if (pass == 2 && !(nw > 0.5 * nprev)) nw = 0.0;
+      nprev = nw;
+    }
+    for (int r = tid; r < m; r += PQR_NT) {
+      const double q = w[r] / nw;
+      w[r] = q;
+      Q[(size_t)kb * ldq + r] = q;
+    }
+    __syncthreads();
+    // W <- W - q (q^T W); recompute column norms; W[:, j] = 0
+    for (int c = warp; c < nc; c += NW) {
+      double* col = W + (size_t)c * ldw;
+      if (c == j) {
+        for (int r = lane; r < m; r += 32) col[r] = 0.0;
+        if (lane == 0) norms[c] = 0.0;
+        continue;
+      }
+      double s = 0.0;
+      for (int r = lane; r < m; r += 32) s += w[r] * col[r];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      double n2 = 0.0;
+      for (int r = lane; r < m; r += 32) {
+        const double x = col[r] - s * w[r];
+        col[r] = x;
+        n2 += x * x;
+      }
+      for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+      if (lane == 0) norms[c] = n2;
+    }
+    __syncthreads();
+    ++t;
+  }
+  if (tid == 0) {
+    if (t_trunc < 0) t_trunc = t;
+    if (tk.t_trunc) *tk.t_trunc = t_trunc;
+    if (tk.t_taken) *tk.t_taken = t;
+  }
+}
+
+// ------------------------------------------------------------------------------ kernel entries
+__global__ void keval_tasks_kernel(const KEvalTask* __restrict__ tasks, const double* __restrict__ pts,
+                                   KernelParams kp, int* __restrict__ flag) {
+  const KEvalTask tk = tasks[blockIdx.x];
+  const int tot = tk.nr * tk.nc;
+  for (int e = threadIdx.x + blockIdx.y * blockDim.x; e < tot; e += blockDim.x * gridDim.y) {
+    const int i = e % tk.nr, j = e / tk.nr;
+    const int gi = tk.rows ? tk.rows[i] : tk.row0 + i;
+    const int gj = tk.cols ? tk.cols[j] : tk.col0 + j;
+    const double v = kernel_entry(kp, pts, gi, gj);
+    if (!isfinite(v)) *flag = 1;
+    tk.out[(size_t)j * tk.ld + i] = v;
+  }
+}
+
+// ------------------------------------------------------------------------------ copies, norms
+__global__ void copy_tasks_kernel(const CopyTask* __restrict__ tasks) {
+  const CopyTask tk = tasks[blockIdx.x];
+  const int tot = tk.rows * tk.cols;
+  for (int e = threadIdx.x + blockIdx.y * blockDim.x; e < tot; e += blockDim.x * gridDim.y) {
+    const int r = e % tk.rows, c = e / tk.rows;
+    double v = tk.alpha;
+    if (tk.src) v *= tk.trans ? tk.src[(size_t)r * tk.lds + c] : tk.src[(size_t)c * tk.lds + r];
+    double* d = tk.dst + (size_t)c * tk.ldd + r;
+    *d = tk.accumulate ? *d + v : v;
+  }
+}
+
+__global__ void norm_tasks_kernel(const NormTask* __restrict__ tasks) {
+  const NormTask tk = tasks[blockIdx.x];
+  __shared__ double red[32];
+  double s = 0.0;
+  const int tot = tk.rows * tk.cols;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const double x = tk.A[(size_t)(e / tk.rows) * tk.lda + (e % tk.rows)];
+    s += x * x;
+  }
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) *tk.out = sqrt(s);
+}
+
+// ------------------------------------------------------------------------------ host launchers
+void launch_gemm(int tileclass, const GemmTask* t, const GemmTerm* tm, const GemmTile* tiles, int ntiles,
+                 cudaStream_t s) {
+  switch (tileclass) {
+    case 0: LAUNCH((gemm_tasks_kernel<32, 32>), ntiles, 32, 0, s, t, tm, tiles); break;
+    case 1: LAUNCH((gemm_tasks_kernel<64, 32>), ntiles, 64, 0, s, t, tm, tiles); break;
+    case 2: LAUNCH((gemm_tasks_kernel<32, 64>), ntiles, 64, 0, s, t, tm, tiles); break;
+    default: LAUNCH((gemm_tasks_kernel<64, 64>), ntiles, 128, 0, s, t, tm, tiles); break;
+  }
+}
+
+void launch_gj(const GJTask* t, int ntasks, int nmax, int mode, cudaStream_t s) {
+  // nmax here is the largest n*ncols (small kernel) or n (global kernel, negative)
+  if (nmax >= 0) {
+    size_t smem = (size_t)nmax * sizeof(double) + 0;  // caller passes n*nc + n + n/2 doubles
+    if (smem > 48 * 1024)
+      AIFMM_CUDA(cudaFuncSetAttribute(gj_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LAUNCH(gj_small_kernel, ntasks, GJ_NT, smem, s, t, mode);
+  } else {
+    size_t smem = (size_t)(-nmax) * (sizeof(double) + sizeof(int));
+    if (smem > 48 * 1024)
+      AIFMM_CUDA(cudaFuncSetAttribute(gj_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LAUNCH(gj_global_kernel, ntasks, GJ_NT, smem, s, t, mode);
+  }
+}
+
+void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s) {
+  LAUNCH(gj_panel_kernel, ntasks, GJ_NT, 0, s, static_cast<const GJBTask*>(t), j);
+}
+void launch_gj_unscramble(const void* t, int ntasks, cudaStream_t s) {
+  LAUNCH(gj_unscramble_kernel, ntasks, 256, 0, s, static_cast<const GJBTask*>(t));
+}
+size_t gjb_task_size() { return sizeof(GJBTask); }
+void gjb_make(void* out, double* A, int lda, int n, double* PW, double* Bws, int* piv, int* info) {
+  GJBTask* t = static_cast<GJBTask*>(out);
+  *t = GJBTask{A, lda, n, PW, Bws, piv, info};
+}
+
+void launch_pqr(const PqrTask* t, int ntasks, size_t smem_doubles, cudaStream_t s) {
+  size_t smem = smem_doubles * sizeof(double);
+  AIFMM_REQUIRE(smem <= 227 * 1024, AIFMM_EOOM, "pivoted QR candidate matrix too wide for shared memory");
+  if (smem > 48 * 1024)
+    AIFMM_CUDA(cudaFuncSetAttribute(pqr_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  LAUNCH(pqr_tasks_kernel, ntasks, PQR_NT, smem, s, t);
+}
+
+void launch_keval(const KEvalTask* t, int ntasks, int ysplit, const double* pts, KernelParams kp, int* flag,
+                  cudaStream_t s) {
+  if (ntasks <= 0) return;
+  dim3 g(ntasks, ysplit);
+  keval_tasks_kernel<<<g, 256, 0, s>>>(t, pts, kp, flag);
+  AIFMM_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_copy(const CopyTask* t, int ntasks, int ysplit, cudaStream_t s) {
+  if (ntasks <= 0) return;
+  dim3 g(ntasks, ysplit);
+  copy_tasks_kernel<<<g, 256, 0, s>>>(t);
+  AIFMM_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_norm(const NormTask* t, int ntasks, cudaStream_t s) { LAUNCH(norm_tasks_kernel, ntasks, 256, 0, s, t); }
+
+}  // namespace aifmm

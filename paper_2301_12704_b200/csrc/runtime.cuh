@@ -1,0 +1,299 @@
+// runtime.cuh — host-side runtime pieces of libaifmm: device pools, task upload arena, batch builders.
+#pragma once
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <set>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace aifmm {
+
+// launchers (dense_kernels.cu, tree_kernels.cu, nnca_kernels.cu)
+void launch_gemm(int tileclass, const GemmTask* t, const GemmTerm* tm, const GemmTile* tiles, int ntiles, cudaStream_t s);
+void launch_gj(const GJTask* t, int ntasks, int nmax, int mode, cudaStream_t s);
+void launch_pqr(const PqrTask* t, int ntasks, size_t smem_doubles, cudaStream_t s);
+void launch_keval(const KEvalTask* t, int ntasks, int ysplit, const double* pts, KernelParams kp, int* flag, cudaStream_t s);
+void launch_copy(const CopyTask* t, int ntasks, int ysplit, cudaStream_t s);
+void launch_norm(const NormTask* t, int ntasks, cudaStream_t s);
+void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s);
+void launch_gj_unscramble(const void* t, int ntasks, cudaStream_t s);
+size_t gjb_task_size();
+void gjb_make(void* out, double* A, int lda, int n, double* PW, double* Bws, int* piv, int* info);
+constexpr int GJ_SMALL_MAX = 80;   // in-place inverses up to this size run in shared memory
+constexpr int GJ_PANEL = 32;
+
+// ---------------------------------------------------------------------------------- pools
+// Chunked bump allocator of device memory.  Blocks live until reset()/release().
+class DevPool {
+ public:
+  explicit DevPool(size_t chunk = (size_t)256 << 20) : chunk_(chunk) {}
+  ~DevPool() { release(); }
+  void* alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    if (bytes == 0) bytes = 256;
+    if (cur_ < chunks_.size() && used_ + bytes <= sizes_[cur_]) {
+      void* p = static_cast<char*>(chunks_[cur_]) + used_;
+      used_ += bytes;
+      return p;
+    }
+    // next existing chunk large enough, else a new one
+    for (size_t c = cur_ + 1; c < chunks_.size(); ++c) {
+      if (bytes <= sizes_[c]) {
+        cur_ = c;
+        used_ = bytes;
+        return chunks_[c];
+      }
+    }
+    size_t sz = std::max(chunk_, bytes);
+    void* p = nullptr;
+    AIFMM_CUDA(cudaMalloc(&p, sz));
+    chunks_.push_back(p);
+    sizes_.push_back(sz);
+    total_ += sz;
+    cur_ = chunks_.size() - 1;
+    used_ = bytes;
+    return p;
+  }
+  double* d(size_t n) { return static_cast<double*>(alloc(n * sizeof(double))); }
+  int* i(size_t n) { return static_cast<int*>(alloc(n * sizeof(int))); }
+  void reset() { cur_ = 0; used_ = 0; if (chunks_.empty()) cur_ = 0; }
+  void release() {
+    for (void* p : chunks_) cudaFree(p);
+    chunks_.clear();
+    sizes_.clear();
+    cur_ = 0;
+    used_ = 0;
+    total_ = 0;
+  }
+  size_t total() const { return total_; }
+
+ private:
+  size_t chunk_;
+  std::vector<void*> chunks_;
+  std::vector<size_t> sizes_;
+  size_t cur_ = 0, used_ = 0, total_ = 0;
+};
+
+// Pinned host staging + device mirror for task arrays.  An append is copied H2D at once;
+// the region is reused only after sync() (stream synchronised).
+class Uploader {
+ public:
+  void init(cudaStream_t s, size_t cap = (size_t)256 << 20) {
+    s_ = s;
+    grow(cap);
+  }
+  ~Uploader() { free_all(); }
+  void free_all() {
+    if (h_) cudaFreeHost(h_);
+    if (d_) cudaFree(d_);
+    h_ = nullptr;
+    d_ = nullptr;
+    cap_ = used_ = 0;
+  }
+  template <class T>
+  T* put(const T* src, size_t n) {
+    size_t bytes = n * sizeof(T);
+    size_t need = (bytes + 255) & ~(size_t)255;
+    if (need == 0) return nullptr;
+    if (used_ + need > cap_) {
+      sync();
+      if (need > cap_) grow(std::max(need, cap_ * 2));
+    }
+    std::memcpy(h_ + used_, src, bytes);
+    AIFMM_CUDA(cudaMemcpyAsync(d_ + used_, h_ + used_, bytes, cudaMemcpyHostToDevice, s_));
+    T* out = reinterpret_cast<T*>(d_ + used_);
+    used_ += need;
+    return out;
+  }
+  template <class T>
+  T* put(const std::vector<T>& v) { return put(v.data(), v.size()); }
+  // make room for `bytes` of consecutive puts (so a batch never straddles a reset)
+  void reserve(size_t bytes) {
+    bytes += 4096;
+    if (used_ + bytes <= cap_) return;
+    sync();
+    if (bytes > cap_) grow(std::max(bytes, cap_ * 2));
+  }
+  void sync() {
+    AIFMM_CUDA(cudaStreamSynchronize(s_));
+    used_ = 0;
+    ++syncs;
+  }
+  long long syncs = 0;
+
+ private:
+  void grow(size_t cap) {
+    if (h_) { AIFMM_CUDA(cudaStreamSynchronize(s_)); cudaFreeHost(h_); cudaFree(d_); }
+    AIFMM_CUDA(cudaMallocHost(&h_, cap));
+    AIFMM_CUDA(cudaMalloc(&d_, cap));
+    cap_ = cap;
+    used_ = 0;
+  }
+  cudaStream_t s_ = 0;
+  char* h_ = nullptr;
+  char* d_ = nullptr;
+  size_t cap_ = 0, used_ = 0;
+};
+
+// ---------------------------------------------------------------------------------- batches
+struct Blk {
+  double* p = nullptr;
+  int ld = 0, rows = 0, cols = 0;
+  double* at(int r, int c) const { return p + (size_t)c * ld + r; }
+};
+
+struct FlopCounter {
+  double flops = 0.0, bytes = 0.0;
+};
+
+class GemmBatch {
+ public:
+  int task(double* C, int ldc, int M, int N, double beta) {
+    GemmTask t{C, ldc, M, N, beta, (int)terms_.size(), (int)terms_.size()};
+    tasks_.push_back(t);
+    return (int)tasks_.size() - 1;
+  }
+  // term on the LAST task
+  void term(double alpha, const double* A, int lda, int transA, const double* B, int ldb, int transB, int K) {
+    GemmTerm tm{A, B, lda, ldb, K, transA, transB, alpha};
+    terms_.push_back(tm);
+    tasks_.back().term_end = (int)terms_.size();
+  }
+  void add(double alpha, const double* B, int ldb, int transB) { term(alpha, nullptr, 0, 0, B, ldb, transB, 0); }
+  bool empty() const { return tasks_.empty(); }
+  size_t size() const { return tasks_.size(); }
+  void run(Uploader& up, cudaStream_t s, FlopCounter* fc = nullptr) {
+    if (tasks_.empty()) return;
+    std::vector<GemmTile> tl[4];
+    for (size_t t = 0; t < tasks_.size(); ++t) {
+      const GemmTask& k = tasks_[t];
+      if (k.M <= 0 || k.N <= 0) continue;
+      int cls = (k.M <= 32 ? 0 : 1) + (k.N <= 32 ? 0 : 2);
+      // class ids: 0 -> 32x32, 1 -> 64x32, 2 -> 32x64, 3 -> 64x64
+      int bm = (cls & 1) ? 64 : 32, bn = (cls & 2) ? 64 : 32;
+      for (int m0 = 0; m0 < k.M; m0 += bm)
+        for (int n0 = 0; n0 < k.N; n0 += bn) tl[cls].push_back(GemmTile{(int)t, m0, n0, 0});
+      if (fc) {
+        fc->bytes += 8.0 * k.M * k.N * (k.beta != 0.0 ? 2.0 : 1.0);
+        for (int q = k.term_begin; q < k.term_end; ++q) {
+          const GemmTerm& tm = terms_[q];
+          if (tm.A) {
+            fc->flops += 2.0 * k.M * k.N * tm.K;
+            fc->bytes += 8.0 * ((double)k.M * tm.K + (double)tm.K * k.N);
+          } else {
+            fc->flops += (double)k.M * k.N;
+            fc->bytes += 8.0 * k.M * k.N;
+          }
+        }
+      }
+    }
+    size_t need = tasks_.size() * sizeof(GemmTask) + terms_.size() * sizeof(GemmTerm) + 4 * 256;
+    for (int c = 0; c < 4; ++c) need += tl[c].size() * sizeof(GemmTile);
+    up.reserve(need);
+    GemmTask* dt = up.put(tasks_);
+    GemmTerm* dm = terms_.empty() ? nullptr : up.put(terms_);
+    for (int c = 0; c < 4; ++c) {
+      if (tl[c].empty()) continue;
+      GemmTile* dtl = up.put(tl[c]);
+      launch_gemm(c, dt, dm, dtl, (int)tl[c].size(), s);
+    }
+    tasks_.clear();
+    terms_.clear();
+  }
+
+ private:
+  std::vector<GemmTask> tasks_;
+  std::vector<GemmTerm> terms_;
+};
+
+class CopyBatch {
+ public:
+  void copy(const double* src, int lds, double* dst, int ldd, int rows, int cols, double alpha = 1.0, int trans = 0,
+            int accumulate = 0) {
+    if (rows <= 0 || cols <= 0) return;
+    v_.push_back(CopyTask{src, dst, lds, ldd, rows, cols, trans, accumulate, alpha});
+    maxel_ = std::max(maxel_, (long long)rows * cols);
+  }
+  void fill(double* dst, int ldd, int rows, int cols, double value) { copy(nullptr, 0, dst, ldd, rows, cols, value); }
+  bool empty() const { return v_.empty(); }
+  void run(Uploader& up, cudaStream_t s) {
+    if (v_.empty()) return;
+    int ys = (int)std::min<long long>(64, std::max<long long>(1, maxel_ / 4096));
+    launch_copy(up.put(v_), (int)v_.size(), ys, s);
+    v_.clear();
+    maxel_ = 0;
+  }
+
+ private:
+  std::vector<CopyTask> v_;
+  long long maxel_ = 0;
+};
+
+
+// Batched in-place matrix inverse (Gauss-Jordan, partial pivoting; reading R16).
+// Small matrices: one CTA each in shared memory.  Larger: blocked GJ, one panel kernel per
+// 32 columns plus one DMMA GEMM launch for the rank-32 update, batched across matrices.
+struct InvReq {
+  double* A;
+  int lda, n;
+  int* info;
+};
+template <class Pool>
+inline void batched_inverse(const std::vector<InvReq>& reqs, Pool& work, Uploader& up, cudaStream_t s,
+                            FlopCounter* fc = nullptr) {
+  std::vector<GJTask> small;
+  int nsm = 0;
+  std::vector<InvReq> big;
+  for (const InvReq& r : reqs) {
+    if (r.n <= 0) continue;
+    if (r.n <= GJ_SMALL_MAX) {
+      small.push_back(GJTask{r.A, r.lda, r.n, r.n, 0, r.info});
+      nsm = std::max(nsm, r.n);
+    } else {
+      big.push_back(r);
+    }
+    if (fc) fc->flops += 2.0 * (double)r.n * r.n * r.n;
+  }
+  if (!small.empty()) {
+    long long smem_d = (long long)nsm * nsm + nsm + nsm / 2 + 2;
+    launch_gj(up.put(small), (int)small.size(), (int)smem_d, 1, s);
+  }
+  if (big.empty()) return;
+  const size_t tsz = gjb_task_size();
+  std::vector<char> tb(tsz * big.size());
+  std::vector<double*> Bw(big.size());
+  int nmax = 0;
+  for (size_t i = 0; i < big.size(); ++i) {
+    const InvReq& r = big[i];
+    double* PW = work.d((size_t)r.n * GJ_PANEL);
+    Bw[i] = work.d((size_t)r.n * GJ_PANEL);
+    int* piv = work.i(r.n);
+    gjb_make(tb.data() + i * tsz, r.A, r.lda, r.n, PW, Bw[i], piv, r.info);
+    nmax = std::max(nmax, r.n);
+  }
+  const void* dt = up.put(tb.data(), tb.size());
+  for (int j = 0; j < nmax; j += GJ_PANEL) {
+    launch_gj_panel(dt, (int)big.size(), j, s);
+    GemmBatch g;
+    for (size_t i = 0; i < big.size(); ++i) {
+      const InvReq& r = big[i];
+      if (j >= r.n) continue;
+      const int nbw = std::min(GJ_PANEL, r.n - j);
+      if (j > 0) {
+        g.task(r.A, r.lda, j, r.n, 1.0);
+        g.term(-1.0, Bw[i], r.n, 0, r.A + j, r.lda, 0, nbw);
+      }
+      if (j + nbw < r.n) {
+        g.task(r.A + j + nbw, r.lda, r.n - j - nbw, r.n, 1.0);
+        g.term(-1.0, Bw[i] + j + nbw, r.n, 0, r.A + j, r.lda, 0, nbw);
+      }
+    }
+    g.run(up, s);
+  }
+  launch_gj_unscramble(dt, (int)big.size(), s);
+}
+
+}  // namespace aifmm
