@@ -26,7 +26,8 @@ tol_c * ||F||_F and Galerkin redirection A <- U~^*(U A V^* + F) V~, which with o
 bases equals L A R^* + R~^* and zero-pads the other
 M2L, M2M, L2L blocks; R15 equal box ranks |z_i| = |y_i| (needed for a square
 pivot [[K, U],[V^*, 0]]) by extending the shorter side's pivoted QR, capped at m_i;
-R16 pivot inverse G = P_i^{-1} by LU with partial pivoting; R17 (Z_i, y_i) = -G22.
+R16 pivot inverse G = P_i^{-1} by LU with partial pivoting; R17 (Z_i, y_i) = -G22;
+R8b the RRQR runs on the triangular factor of the projected candidate matrix (tri_root).
 """
 from __future__ import annotations
 
@@ -42,6 +43,18 @@ def _pad(M, r, c):
     out = np.zeros((r, c))
     out[:M.shape[0], :M.shape[1]] = M
     return out
+
+
+def tri_root(W):
+    """R8b two-stage RRQR: W^T = Q R (Householder), return R^T (m x min(m, n)).
+
+    For every projector P acting on the left, ||(I - P) R^T||_F = ||(I - P) W||_F and
+    range(R^T) = range(W), so the truncated pivoted QR of R^T is a rank-revealing QR of W
+    with exactly the truncation criterion of R8 -- on an m x m instead of an m x n matrix."""
+    if W.shape[1] == 0:
+        return W
+    R = np.linalg.qr(W.T, mode="r")
+    return np.ascontiguousarray(R.T)
 
 
 def extend_basis(W, B, tau, t):
@@ -178,8 +191,8 @@ class AIFMM:
             FU = np.concatenate([lv.F[(b, q)] for q in ps], axis=1)       # row X_b
             FV = np.concatenate([lv.F[(p, b)].T for p in ps], axis=1)     # column x_b
             nU, nV = np.linalg.norm(FU), np.linalg.norm(FV)
-            WU = FU - lv.U[b] @ (lv.U[b].T @ FU)
-            WV = FV - lv.V[b] @ (lv.V[b].T @ FV)
+            WU = tri_root(FU - lv.U[b] @ (lv.U[b].T @ FU))
+            WV = tri_root(FV - lv.V[b] @ (lv.V[b].T @ FV))
             cap = m - k
             _, tU = pivoted_qr_extend(WU, lv.U[b], self.tol_c * nU, 0, cap)
             _, tV = pivoted_qr_extend(WV, lv.V[b], self.tol_c * nV, 0, cap)

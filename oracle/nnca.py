@@ -11,7 +11,8 @@ Readings: R9 the pivot rule (deferred by P:359 to another paper) is 
 partial pivoting on A(R_B, F_B); R10 u = v and a symmetric kernel give one skeleton
 sk(B) = t^{B,i} = s^{B,o} and one far-pivot set fp(B) = s^{B,i} = t^{B,o}, so V_B = U_B;
 R11 at non-leaf levels the candidate rows R_B are the children's skeletons stacked in
-Morton order (Eq. P:414-416: particles of a parent are its children's multipoles).
+Morton order (Eq. P:414-416: particles of a parent are its children's multipoles); R20 when
+IL(B) holds fewer points than R_B, the ancestors' interaction lists are appended to F_B.
 """
 from __future__ import annotations
 
@@ -101,6 +102,12 @@ class NNCA:
                     parts = [self.sk[l + 1][c] for c in tree.children(l, B)]
                     R = np.concatenate(parts) if parts else np.zeros(0, np.int64)
                 F = [np.arange(*tree.point_range(l, D), dtype=np.int64) for D in il[l][B]]
+                # R20: a sparse neighbourhood can leave IL(B) with fewer points than R_B; then
+                # the IL of the ancestors (coarser far field of B) is appended, parent first
+                la, A_ = l, B
+                while sum(f.size for f in F) < R.size and la > 2:
+                    la, A_ = la - 1, A_ >> tree.d
+                    F += [np.arange(*tree.point_range(la, D), dtype=np.int64) for D in il[la][A_]]
                 F = np.concatenate(F) if F else np.zeros(0, np.int64)
                 self.R[l][B] = R
                 if R.size == 0 or F.size == 0:

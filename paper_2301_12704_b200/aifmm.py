@@ -107,6 +107,11 @@ def solve(B):
     return X[:, 0] if one else X
 
 
+def solve_device_ptr(ptr: int, nrhs: int):
+    """In-place solve of a column-major n x nrhs device buffer given by its address."""
+    _check(load().aifmm_solve(ctypes.c_void_p(ptr), int(nrhs)))
+
+
 def solve_host(B: np.ndarray) -> np.ndarray:
     """End-to-end path: host B (n,) or (n, nrhs) -> host X (copies inside the library)."""
     lib = load()

@@ -60,6 +60,12 @@ __global__ void icopy_kernel(const int* src, int* dst, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     dst[i] = src[i];
 }
+// batched integer copies: task t copies n[t] ints from src[t] (or base[t] + i if src is null)
+struct ICopyTask { const int* src; int* dst; int n, base; };
+__global__ void icopy_tasks_kernel(const ICopyTask* __restrict__ t) {
+  const ICopyTask k = t[blockIdx.x];
+  for (int i = threadIdx.x; i < k.n; i += blockDim.x) k.dst[i] = k.src ? k.src[i] : k.base + i;
+}
 // rows permutation of an N x nrhs column-major matrix: dst[j,:] = src[perm[j],:] (gather) or
 // dst[perm[j],:] = src[j,:] (scatter)
 __global__ void permute_rows_kernel(const double* src, double* dst, const int* perm, long long n, int nrhs, int scatter) {
@@ -224,8 +230,8 @@ static void build_tree(Ctx& c, const double* user_pts) {
   int* dmax = P.i(1);
   int L = -1;
   for (int l = 2; l <= 20; ++l) {
-    AIFMM_REQUIRE(d * l <= 24, AIFMM_EINVALID_ARG,
-                  "cannot subdivide: coincident points or a tree deeper than 2^24 boxes per level");
+    AIFMM_REQUIRE(d * l <= 24, AIFMM_ECOINCIDENT,
+                  "cannot subdivide: more than leaf_size coincident points (tree deeper than 2^24 boxes per level)");
     const int nb = 1 << (d * l);
     int* cnt = c.work.i(nb);
     AIFMM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * nb, c.s));
@@ -308,21 +314,16 @@ static void build_nnca(Ctx& c) {
       nl.Roff[b + 1] = nl.Roff[b] + r;
     }
     nl.dR = c.persist.i(std::max<long long>(nl.Roff[nb], 1));
-    for (int b : boxes) {
-      if (!nl.nR[b]) continue;
-      if (l == L) {
-        LAUNCH(iota_kernel, gsz(nl.nR[b]), 256, 0, c.s, nl.dR + nl.Roff[b], (long long)nl.nR[b], (int)c.off[l][b]);
-      }
-    }
-    if (l < L) {
-      // concatenate children's skeletons (children are consecutive ids, so the concatenation
-      // of children's sk arrays in Morton order is one contiguous copy per parent)
-      const NLevel& cl = c.nn[l + 1];
+    {
+      // leaf rows are point ranges; above, the children's skeletons (children have consecutive
+      // ids, so their sk arrays are one contiguous run per parent)
+      std::vector<ICopyTask> ic;
       for (int b : boxes) {
         if (!nl.nR[b]) continue;
-        long long s0 = cl.skoff[(size_t)b << c.d];
-        LAUNCH(icopy_kernel, gsz(nl.nR[b]), 256, 0, c.s, cl.dsk + s0, nl.dR + nl.Roff[b], (long long)nl.nR[b]);
+        if (l == L) ic.push_back(ICopyTask{nullptr, nl.dR + nl.Roff[b], nl.nR[b], (int)c.off[l][b]});
+        else ic.push_back(ICopyTask{c.nn[l + 1].dsk + c.nn[l + 1].skoff[(size_t)b << c.d], nl.dR + nl.Roff[b], nl.nR[b], 0});
       }
+      if (!ic.empty()) LAUNCH(icopy_tasks_kernel, (int)ic.size(), 128, 0, c.s, c.up.put(ic));
     }
     // far ranges per box
     std::vector<int> fr;
@@ -339,6 +340,19 @@ static void build_nnca(Ctx& c) {
         nF[b] += c.count(l, il[t]);
       }
       froff[b + 1] += ni;
+      // R20: sparse neighbourhoods -> append the ancestors' interaction lists
+      int la = l, ab = b;
+      while (nF[b] < nl.nR[b] && la > 2) {
+        --la;
+        ab >>= c.d;
+        const int* ila = c.ilist(la, ab, &ni);
+        for (int t = 0; t < ni; ++t) {
+          fr.push_back((int)c.off[la][ila[t]]);
+          fr.push_back((int)c.off[la][ila[t] + 1]);
+          nF[b] += c.count(la, ila[t]);
+        }
+        froff[b + 1] += ni;
+      }
     }
     int* dfr = fr.empty() ? nullptr : c.up.put(fr);
     // ACA in chunks bounded by workspace
@@ -397,10 +411,14 @@ static void build_nnca(Ctx& c) {
     for (int b = 0; b < nb; ++b) nl.skoff[b + 1] = nl.skoff[b] + nl.k[b];
     nl.dsk = c.persist.i(std::max<long long>(nl.skoff[nb], 1));
     nl.dfp = c.persist.i(std::max<long long>(nl.skoff[nb], 1));
-    for (int b : boxes) {
-      if (!nl.k[b]) continue;
-      LAUNCH(icopy_kernel, gsz(nl.k[b]), 256, 0, c.s, drp + pivoff[b], nl.dsk + nl.skoff[b], (long long)nl.k[b]);
-      LAUNCH(icopy_kernel, gsz(nl.k[b]), 256, 0, c.s, dcp + pivoff[b], nl.dfp + nl.skoff[b], (long long)nl.k[b]);
+    {
+      std::vector<ICopyTask> ic;
+      for (int b : boxes) {
+        if (!nl.k[b]) continue;
+        ic.push_back(ICopyTask{drp + pivoff[b], nl.dsk + nl.skoff[b], nl.k[b], 0});
+        ic.push_back(ICopyTask{dcp + pivoff[b], nl.dfp + nl.skoff[b], nl.k[b], 0});
+      }
+      if (!ic.empty()) LAUNCH(icopy_tasks_kernel, (int)ic.size(), 128, 0, c.s, c.up.put(ic));
     }
     // operators: [A(fp,sk) | A(fp,R)] -> [I | X] by Gauss-Jordan (a solve, not an explicit
     // inverse: A(fp,sk) can be ill-conditioned), U = X^T (R10: V = U)
@@ -605,7 +623,7 @@ static void orthonormalise(Ctx& c, FLevel& f) {
     smem = std::max(smem, (size_t)k + m + k);
   }
   cb.run(c.up, c.s);
-  if (!pq.empty()) launch_pqr(c.up.put(pq), (int)pq.size(), smem, c.s);
+  if (!pq.empty()) run_pqr(pq, c.up, c.s);
   GemmBatch g;
   for (int b : f.boxes) {
     const int m = f.m[b], k = f.k[b];
@@ -682,7 +700,9 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   }
   const int na = (int)aff.size();
   if (!na) return;
-  struct Side { double* W; int nc; };
+  if (g_prof.on) g_prof.begin(c.s);
+  // candidates stored transposed (rows = fill-in columns): WT_U = [F_bq^T ...], WT_V = [F_pb ...]
+  struct Side { double* WT; int n; double* M; int r; };
   std::vector<Side> su(na), sv(na);
   double* dnorm = c.work.d(2 * na);
   int* dt = c.work.i(4 * na);
@@ -691,61 +711,83 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
     const int m = f.m[b];
-    int ncu = 0, ncv = 0;
-    for (int q : part[b]) { ncu += live(f, q); ncv += live(f, q); }
-    su[a] = Side{c.work.d((size_t)m * std::max(ncu, 1)), ncu};
-    sv[a] = Side{c.work.d((size_t)m * std::max(ncv, 1)), ncv};
-    int ou = 0, ov = 0;
+    int nu = 0;
+    for (int q : part[b]) nu += live(f, q);
+    su[a].n = sv[a].n = nu;
+    su[a].WT = c.work.d((size_t)std::max(nu, 1) * m);
+    sv[a].WT = c.work.d((size_t)std::max(nu, 1) * m);
+    su[a].r = sv[a].r = std::min(nu, m);
+    su[a].M = c.work.d((size_t)m * std::max(su[a].r, 1));
+    sv[a].M = c.work.d((size_t)m * std::max(sv[a].r, 1));
+    int o = 0;
     for (int q : part[b]) {
-      const Blk& fb = f.F.at(f.key(b, q));   // row X_b, column of q
-      cb.copy(fb.p, fb.ld, su[a].W + (size_t)ou * m, m, m, live(f, q));
-      ou += live(f, q);
-      const Blk& gb = f.F.at(f.key(q, b));   // row of q, column x_b -> transposed
-      cb.copy(gb.p, gb.ld, sv[a].W + (size_t)ov * m, m, m, live(f, q), 1.0, /*trans=*/1);
-      ov += live(f, q);
+      const Blk& fb = f.F.at(f.key(b, q));   // row X_b, column of q: m x live_q -> transposed
+      cb.copy(fb.p, fb.ld, su[a].WT + o, nu, live(f, q), m, 1.0, /*trans=*/1);
+      const Blk& gb = f.F.at(f.key(q, b));   // row of q, column x_b: live_q x m (already W^T rows)
+      cb.copy(gb.p, gb.ld, sv[a].WT + o, nu, live(f, q), m);
+      o += live(f, q);
     }
-    nt.push_back(NormTask{su[a].W, m, m, ncu, dnorm + 2 * a});
-    nt.push_back(NormTask{sv[a].W, m, m, ncv, dnorm + 2 * a + 1});
+    nt.push_back(NormTask{su[a].WT, std::max(nu, 1), nu, m, dnorm + 2 * a});
+    nt.push_back(NormTask{sv[a].WT, std::max(nu, 1), nu, m, dnorm + 2 * a + 1});
   }
   cb.run(c.up, c.s);
   launch_norm(c.up.put(nt), (int)nt.size(), c.s);
-  // projection W -= B (B^T W)
+  if (g_prof.on) { g_prof.end("cmp.gather"); g_prof.begin(c.s); }
+  // projection W <- (I - B B^T) W, i.e. WT <- WT - (WT B) B^T
   GemmBatch g;
   std::vector<double*> tu(na), tv(na);
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
-    const int m = f.m[b], k = f.k[b];
-    if (!k) continue;
-    tu[a] = c.work.d((size_t)k * std::max(su[a].nc, 1));
-    tv[a] = c.work.d((size_t)k * std::max(sv[a].nc, 1));
-    g.task(tu[a], k, k, su[a].nc, 0.0);
-    g.term(1.0, f.U[b], m, 1, su[a].W, m, 0, m);
-    g.task(tv[a], k, k, sv[a].nc, 0.0);
-    g.term(1.0, f.V[b], m, 1, sv[a].W, m, 0, m);
+    const int m = f.m[b], k = f.k[b], nu = su[a].n;
+    if (!k || !nu) continue;
+    tu[a] = c.work.d((size_t)nu * k);
+    tv[a] = c.work.d((size_t)nu * k);
+    g.task(tu[a], nu, nu, k, 0.0);
+    g.term(1.0, su[a].WT, nu, 0, f.U[b], m, 0, m);
+    g.task(tv[a], nu, nu, k, 0.0);
+    g.term(1.0, sv[a].WT, nu, 0, f.V[b], m, 0, m);
   }
   g.run(c.up, c.s, &c.fc_all);
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
-    const int m = f.m[b], k = f.k[b];
-    if (!k) continue;
-    g.task(su[a].W, m, m, su[a].nc, 1.0);
-    g.term(-1.0, f.U[b], m, 0, tu[a], k, 0, k);
-    g.task(sv[a].W, m, m, sv[a].nc, 1.0);
-    g.term(-1.0, f.V[b], m, 0, tv[a], k, 0, k);
+    const int m = f.m[b], k = f.k[b], nu = su[a].n;
+    if (!k || !nu) continue;
+    g.task(su[a].WT, nu, nu, m, 1.0);
+    g.term(-1.0, tu[a], nu, 0, f.U[b], m, 1, k);
+    g.task(sv[a].WT, nu, nu, m, 1.0);
+    g.term(-1.0, tv[a], nu, 0, f.V[b], m, 1, k);
   }
   g.run(c.up, c.s, &c.fc_all);
+  // two-stage RRQR (R8b): M = R^T with WT = Q R
+  std::vector<TriRootReq> tr;
+  for (int a = 0; a < na; ++a) {
+    int b = aff[a];
+    const int m = f.m[b], nu = su[a].n;
+    if (!nu || !m) continue;
+    tr.push_back(TriRootReq{su[a].WT, nu, nu, m, su[a].M, m});
+    tr.push_back(TriRootReq{sv[a].WT, nu, nu, m, sv[a].M, m});
+  }
+  batched_tri_root(tr, c.work, c.up, c.s, &c.fc_all);
+  if (g_prof.on) { g_prof.end("cmp.proj+triroot"); g_prof.begin(c.s); }
+  struct SideW { double* W; int nc; };
+  std::vector<SideW> wu(na), wv(na);
+  for (int a = 0; a < na; ++a) {
+    wu[a] = SideW{su[a].M, su[a].r};
+    wv[a] = SideW{sv[a].M, sv[a].r};
+  }
   // phase A: truncated pivoted QR on both sides
   std::vector<PqrTask> pq;
   size_t smem = 0;
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
     const int m = f.m[b], k = f.k[b];
-    pq.push_back(PqrTask{su[a].W, f.U[b], m, m, m, su[a].nc, k, 0, m - k, 0, dnorm + 2 * a, c.tol_c, dt + 4 * a, dt + 4 * a + 1});
-    pq.push_back(PqrTask{sv[a].W, f.V[b], m, m, m, sv[a].nc, k, 0, m - k, 0, dnorm + 2 * a + 1, c.tol_c, dt + 4 * a + 2, dt + 4 * a + 3});
-    smem = std::max(smem, (size_t)std::max(su[a].nc, sv[a].nc) + m + m);
+    pq.push_back(PqrTask{wu[a].W, f.U[b], m, m, m, wu[a].nc, k, 0, m - k, 0, dnorm + 2 * a, c.tol_c, dt + 4 * a, dt + 4 * a + 1});
+    pq.push_back(PqrTask{wv[a].W, f.V[b], m, m, m, wv[a].nc, k, 0, m - k, 0, dnorm + 2 * a + 1, c.tol_c, dt + 4 * a + 2, dt + 4 * a + 3});
+    smem = std::max(smem, (size_t)std::max(wu[a].nc, wv[a].nc) + m + m);
   }
-  launch_pqr(c.up.put(pq), (int)pq.size(), smem, c.s);
+  run_pqr(pq, c.up, c.s);
   std::vector<int> th = d2h(c, dt, 4 * na);
+  if (g_prof.on) { g_prof.end("cmp.pqrA"); g_prof.begin(c.s); }
   std::vector<int> tgt(na), hu(na), hv(na);
   pq.clear();
   smem = 0;
@@ -756,17 +798,17 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
     hv[a] = th[4 * a + 3];
     tgt[a] = std::min(std::max(th[4 * a], th[4 * a + 2]), m - k);
     if (hu[a] < tgt[a])
-      pq.push_back(PqrTask{su[a].W, f.U[b], m, m, m, su[a].nc, k + hu[a], tgt[a] - hu[a], tgt[a] - hu[a], 0, nullptr, 0.0,
+      pq.push_back(PqrTask{wu[a].W, f.U[b], m, m, m, wu[a].nc, k + hu[a], tgt[a] - hu[a], tgt[a] - hu[a], 0, nullptr, 0.0,
                            nullptr, dt + 4 * a + 1});
     if (hv[a] < tgt[a])
-      pq.push_back(PqrTask{sv[a].W, f.V[b], m, m, m, sv[a].nc, k + hv[a], tgt[a] - hv[a], tgt[a] - hv[a], 0, nullptr, 0.0,
+      pq.push_back(PqrTask{wv[a].W, f.V[b], m, m, m, wv[a].nc, k + hv[a], tgt[a] - hv[a], tgt[a] - hv[a], 0, nullptr, 0.0,
                            nullptr, dt + 4 * a + 3});
-    smem = std::max(smem, (size_t)std::max(su[a].nc, sv[a].nc) + m + m);
+    smem = std::max(smem, (size_t)std::max(wu[a].nc, wv[a].nc) + m + m);
   }
   std::vector<int> haveU = hu, haveV = hv;
   if (!pq.empty()) {
     // phase B: continue the shorter side past its truncation point (R15)
-    launch_pqr(c.up.put(pq), (int)pq.size(), smem, c.s);
+    run_pqr(pq, c.up, c.s);
     th = d2h(c, dt, 4 * na);
     for (int a = 0; a < na; ++a) {
       if (hu[a] < tgt[a]) haveU[a] = hu[a] + th[4 * a + 1];
@@ -807,7 +849,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
       }
     }
     if (!pi.empty()) {
-      launch_pqr(c.up.put(pi), (int)pi.size(), smem2, c.s);
+      run_pqr(pi, c.up, c.s);
       th = d2h(c, dt, 4 * na);
       for (auto& w : who) {
         if (w.second) haveV[w.first] += th[4 * w.first + 3];
@@ -817,6 +859,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   }
   for (int a = 0; a < na; ++a)
     AIFMM_REQUIRE(haveU[a] == tgt[a] && haveV[a] == tgt[a], AIFMM_ESINGULAR_PIVOT, "rank equalisation failed");
+  if (g_prof.on) { g_prof.end("cmp.pqrB"); g_prof.begin(c.s); }
   // new ranks
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
@@ -864,6 +907,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   g.run(c.up, c.s, &c.fc_all);
   cb.run(c.up, c.s);
   for (auto& pr : S) f.pending.erase(pr);
+  if (g_prof.on) g_prof.end("cmp.redirect");
 }
 
 static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
@@ -915,6 +959,7 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
     }
   }
   g.run(c.up, c.s, &c.fc_all);
+  if (g_prof.on) { g_prof.end("elim.W"); g_prof.begin(c.s); }
   // 3. Schur updates, target-centric (deterministic ascending-i accumulation), + new blocks
   std::map<std::pair<int, int>, std::vector<int>> targets;   // (p,q) -> list of a (index into cs)
   for (size_t a = 0; a < cs.size(); ++a)
@@ -977,7 +1022,7 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
     AIFMM_CUDA(cudaEventCreate(&e1));
     AIFMM_CUDA(cudaEventRecord(e0, c.s));
   }
-  if (g_prof.on) { g_prof.end("elim.W+plan"); g_prof.begin(c.s); }
+  if (g_prof.on) { g_prof.end("elim.plan"); g_prof.begin(c.s); }
   long long l0 = g_launches;
   g.run(c.up, c.s, &c.fc_schur);
   c.stats[AIFMM_STAT_SCHUR_LAUNCHES] += (double)(g_launches - l0);
@@ -1020,12 +1065,19 @@ static void factor_all(Ctx& c) {
         if (c.col[l][pr.first] == col || c.col[l][pr.second] == col) S.push_back(pr);
       g_prof.begin(c.s);
       if (!S.empty()) compress(c, f, S);
-      g_prof.end("compress");
+      g_prof.end(("compress.L" + std::to_string(l)).c_str());
       g_prof.begin(c.s);
       eliminate_colour(c, f, cs);
-      g_prof.end("eliminate");
+      g_prof.end(("eliminate.L" + std::to_string(l)).c_str());
     }
     AIFMM_REQUIRE(f.pending.empty(), AIFMM_ESINGULAR_PIVOT, "pending far fill-ins at level end");
+    if (g_prof.on) {
+      double ms = 0, mx = 0, ks = 0, kx = 0, k0s = 0;
+      for (int b : f.boxes) { ms += f.m[b]; mx = std::max(mx, (double)f.m[b]); ks += f.k[b]; kx = std::max(kx, (double)f.k[b]); k0s += c.nn[l].k[b]; }
+      double nbx = (double)f.boxes.size();
+      fprintf(stderr, "[aifmm profile] level %d boxes %d m avg %.1f max %.0f | k nnca avg %.1f final avg %.1f max %.0f\n",
+              l, (int)nbx, ms / nbx, mx, k0s / nbx, ks / nbx, kx);
+    }
     for (int b : f.boxes) c.stats[AIFMM_STAT_MAX_RANK] = std::max(c.stats[AIFMM_STAT_MAX_RANK], (double)f.k[b]);
     // solve layout
     f.xrow.assign(f.nb + 1, 0);

@@ -42,6 +42,16 @@ extern long long g_launches;
     }                                                                 \
   } while (0)
 
+// Raise a kernel's dynamic shared-memory limit when a launch needs more than it allows
+// (the default allowance is 48 KB minus the kernel's static shared memory).
+template <class F>
+inline void ensure_dyn_smem(F* func, size_t bytes) {
+  cudaFuncAttributes fa{};
+  AIFMM_CUDA(cudaFuncGetAttributes(&fa, func));
+  if ((int)bytes > fa.maxDynamicSharedSizeBytes)
+    AIFMM_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
 // ---------------------------------------------------------------------------------------
 // Task records (built on the host by the planner, uploaded, consumed by batched kernels).
 // All matrices are column-major; "ld" is the leading dimension.

@@ -10,7 +10,12 @@
 //   pqr_tasks_kernel   : column-pivoted Gram-Schmidt with truncation (the paper's RRQR).
 //   keval_tasks_kernel : kernel-entry blocks A(rows, cols).
 //   copy/norm kernels  : block assembly, level transition gathers, Frobenius norms.
+#include <cooperative_groups.h>
+#include <cstdio>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace aifmm {
 
@@ -276,14 +281,15 @@ struct GJBTask {
   int* info;
 };
 
-__global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restrict__ tasks, int j) {
+__global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restrict__ tasks, int j, int smem_elems) {
+  extern __shared__ double gj_pw_smem[];
   const GJBTask tk = tasks[blockIdx.x];
   const int n = tk.n;
   if (j >= n) return;
   if (*tk.info) return;
   const int nbw = min(GJB, n - j), rows = n - j, ld = tk.lda;
   double* A = tk.A;
-  double* PW = tk.PW;
+  double* PW = (rows * nbw <= smem_elems) ? gj_pw_smem : tk.PW;   // panel LU in smem when it fits
   __shared__ double red[32];
   __shared__ int redi[32];
   __shared__ double Li[GJB][GJB + 1], Ui[GJB][GJB + 1], Di[GJB][GJB + 1];
@@ -511,6 +517,509 @@ __global__ void __launch_bounds__(PQR_NT) pqr_tasks_kernel(const PqrTask* __rest
   }
 }
 
+// Cluster variant of the pivoted QR (same decision rule and arithmetic order per column as
+// pqr_tasks_kernel): the 8 CTAs of a cluster own contiguous column slices of W (staged in
+// shared memory when they fit), the pivot search / residual sums / re-orthogonalisation
+// coefficients are combined through DSMEM, and the re-orthogonalisation is row-split.
+constexpr int PQC = 8;
+__global__ void __cluster_dims__(PQC, 1, 1) __launch_bounds__(PQR_NT)
+pqr_cluster_kernel(const PqrTask* __restrict__ tasks, int smem_cap) {
+  extern __shared__ double pqs[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const PqrTask tk = tasks[blockIdx.x / PQC];
+  const int m = tk.m, nc = tk.ncols, ldq = tk.ldq;
+  const int cw = (nc + PQC - 1) / PQC;
+  const int c0 = min(nc, rank * cw), c1 = min(nc, c0 + cw), ncl = c1 - c0;
+  const int kmax = tk.k0 + tk.tmax;
+  // shared layout: w[m] | coef[kmax] | norms[cw] | Wl[m*cw] (if staged)
+  double* w = pqs;
+  double* coef = w + m;
+  double* norms = coef + kmax;
+  double* Wst = norms + cw;
+  const bool staged = (size_t)(m + kmax + cw) + (size_t)m * cw <= (size_t)smem_cap;
+  double* Wl = staged ? Wst : tk.W + (size_t)c0 * tk.ldw;
+  const int ldl = staged ? m : tk.ldw;
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  __shared__ double s_part, s_max;
+  __shared__ int s_idx;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = PQR_NT / 32;
+  const double tau = tk.tol * (tk.fnorm ? *tk.fnorm : 1.0);
+  double* Q = tk.Q;
+  if (staged)
+    for (int e = tid; e < m * ncl; e += PQR_NT) Wl[(size_t)(e / m) * ldl + e % m] = tk.W[(size_t)(c0 + e / m) * tk.ldw + e % m];
+  __syncthreads();
+  for (int c = warp; c < ncl; c += NW) {
+    double sacc = 0.0;
+    for (int r = lane; r < m; r += 32) { const double x = Wl[(size_t)c * ldl + r]; sacc += x * x; }
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) norms[c] = sacc;
+  }
+  __syncthreads();
+  // row slice for the re-orthogonalisation
+  const int rw = (m + PQC - 1) / PQC;
+  const int r0 = min(m, rank * rw), r1 = min(m, r0 + rw);
+  int t = 0, t_trunc = -1;
+  while (true) {
+    double part = 0.0;
+    for (int c = tid; c < ncl; c += PQR_NT) part += norms[c];
+    part = block_sum<PQR_NT>(part, red);
+    if (tid == 0) s_part = part;
+    cl.sync();
+    double res2 = 0.0;
+    for (int q = 0; q < PQC; ++q) res2 += *cl.map_shared_rank(&s_part, q);
+    const bool ok = !(sqrt(res2) > tau);
+    if (ok && t_trunc < 0) t_trunc = t;
+    if ((t >= tk.tmin && ok) || t >= tk.tmax) break;
+    double v = -1.0;
+    for (int c = tid; c < ncl; c += PQR_NT) v = fmax(v, sqrt(norms[c]));
+    v = block_max<PQR_NT>(v, red);
+    if (tid == 0) s_max = v;
+    cl.sync();
+    double mx = -1.0;
+    for (int q = 0; q < PQC; ++q) mx = fmax(mx, *cl.map_shared_rank(&s_max, q));
+    if (!(mx > 0.0)) break;
+    const double thr = mx * (1.0 - TIE);
+    int cand = 0x7fffffff;
+    for (int c = tid; c < ncl; c += PQR_NT)
+      if (sqrt(norms[c]) >= thr) { cand = c0 + c; break; }
+    cand = block_min_int<PQR_NT>(cand, redi);
+    if (tid == 0) s_idx = cand;
+    cl.sync();
+    int j = 0x7fffffff;
+    for (int q = 0; q < PQC; ++q) j = min(j, *cl.map_shared_rank(&s_idx, q));
+    const int jo = min(PQC - 1, j / cw);       // owner rank of column j
+    // fetch column j (owner's slice) into w
+    {
+      const double* src = (staged ? cl.map_shared_rank(Wst, jo) : tk.W + (size_t)(jo * cw) * tk.ldw);
+      const int lds = staged ? m : tk.ldw;
+      const int lj = j - jo * cw;
+      for (int r = tid; r < m; r += PQR_NT) w[r] = src[(size_t)lj * lds + r];
+    }
+    __syncthreads();
+    const int kb = tk.k0 + t;
+    double nprev = 0.0, nw = 0.0;
+    for (int pass = 0; pass < 3; ++pass) {
+      // coefficients for basis vectors s in this rank's slice of [0, kb)
+      const int sw = (kb + PQC - 1) / PQC;
+      const int s0 = min(kb, rank * sw), s1 = min(kb, s0 + sw);
+      for (int sidx = s0 + warp; sidx < s1; sidx += NW) {
+        double acc = 0.0;
+        for (int r = lane; r < m; r += 32) acc += Q[(size_t)sidx * ldq + r] * w[r];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) coef[sidx] = acc;
+      }
+      cl.sync();
+      // gather all coefficients
+      for (int sidx = tid; sidx < kb; sidx += PQR_NT) {
+        const int own = min(PQC - 1, sidx / max(sw, 1));
+        if (own != rank) coef[sidx] = cl.map_shared_rank(coef, own)[sidx];
+      }
+      cl.sync();
+      // own row slice of w -= Q coef
+      double p2 = 0.0;
+      for (int r = r0 + tid; r < r1; r += PQR_NT) {
+        double acc = w[r];
+        for (int sidx = 0; sidx < kb; ++sidx) acc -= Q[(size_t)sidx * ldq + r] * coef[sidx];
+        w[r] = acc;
+        p2 += acc * acc;
+      }
+      p2 = block_sum<PQR_NT>(p2, red);
+      if (tid == 0) s_part = p2;
+      cl.sync();
+      double n2 = 0.0;
+      for (int q = 0; q < PQC; ++q) n2 += *cl.map_shared_rank(&s_part, q);
+      // gather the full w from the row owners
+      for (int r = tid; r < m; r += PQR_NT) {
+        const int own = min(PQC - 1, r / max(rw, 1));
+        if (own != rank) w[r] = cl.map_shared_rank(w, own)[r];
+      }
+      cl.sync();
+      nw = sqrt(n2);
+      if (pass == 1 && nw > 0.5 * nprev) break;
+      if (pass == 2 && !(nw > 0.5 * nprev)) nw = 0.0;
+      nprev = nw;
+    }
+    if (!(nw > 0.0)) {
+      if (j >= c0 && j < c1) {
+        for (int r = tid; r < m; r += PQR_NT) Wl[(size_t)(j - c0) * ldl + r] = 0.0;
+        if (tid == 0) norms[j - c0] = 0.0;
+      }
+      __syncthreads();
+      cl.sync();
+      continue;
+    }
+    for (int r = tid; r < m; r += PQR_NT) {
+      const double qv = w[r] / nw;
+      w[r] = qv;
+      if (rank == 0) Q[(size_t)kb * ldq + r] = qv;
+    }
+    __syncthreads();
+    for (int c = warp; c < ncl; c += NW) {
+      double* col = Wl + (size_t)c * ldl;
+      if (c0 + c == j) {
+        for (int r = lane; r < m; r += 32) col[r] = 0.0;
+        if (lane == 0) norms[c] = 0.0;
+        continue;
+      }
+      double sacc = 0.0;
+      for (int r = lane; r < m; r += 32) sacc += w[r] * col[r];
+      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+      double n2 = 0.0;
+      for (int r = lane; r < m; r += 32) {
+        const double x = col[r] - sacc * w[r];
+        col[r] = x;
+        n2 += x * x;
+      }
+      for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+      if (lane == 0) norms[c] = n2;
+    }
+    __syncthreads();
+    cl.sync();
+    ++t;
+  }
+  if (staged)
+    for (int e = tid; e < m * ncl; e += PQR_NT) tk.W[(size_t)(c0 + e / m) * tk.ldw + e % m] = Wl[(size_t)(e / m) * ldl + e % m];
+  if (rank == 0 && tid == 0) {
+    if (t_trunc < 0) t_trunc = t;
+    if (tk.t_trunc) *tk.t_trunc = t_trunc;
+    if (tk.t_taken) *tk.t_taken = t;
+  }
+  cl.sync();
+}
+
+// ------------------------------------------------------------------------------ Householder QR
+// Blocked Householder QR of a batch of tall n x m matrices A (column-major, lda), used for the
+// first stage of the two-stage RRQR (reading R8b): W^T = Q R, then pivoted QR of R^T.
+// Panel kernel: unblocked Householder (LAPACK dlarfg convention) on columns [j, j+nbw) and
+// rows [j, n), explicit V (unit diagonal) and the compact-WY factor T (dlarft, forward);
+// the trailing update (I - V T^T V^T) C is three DMMA GEMM launches issued by the host.
+constexpr int HHB = 32;
+struct HHTask {
+  double* A;
+  int lda, n, m;
+  double* V;     // workspace n x HHB (ld n)
+  double* T;     // workspace HHB x HHB (ld HHB)
+};
+
+__global__ void __launch_bounds__(256) hh_panel_kernel(const HHTask* __restrict__ tasks, int j) {
+  const HHTask tk = tasks[blockIdx.x];
+  const int r = min(tk.n, tk.m);
+  if (j >= r) return;
+  const int nbw = min(HHB, r - j), rows = tk.n - j, ld = tk.lda;
+  double* A = tk.A + j + (size_t)j * ld;   // panel origin
+  __shared__ double red[32];
+  __shared__ double tau_s[HHB];
+  __shared__ double G[HHB][HHB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = 0; c < nbw; ++c) {
+    double* x = A + (size_t)c * ld + c;     // column c, from the diagonal down
+    const int len = rows - c;
+    double p = 0.0;
+    for (int i = 1 + tid; i < len; i += 256) p += x[i] * x[i];
+    const double sigma = block_sum<256>(p, red);
+    const double alpha = x[0];
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (sigma > 0.0) {
+      const double nrm = sqrt(alpha * alpha + sigma);
+      beta = (alpha >= 0.0) ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    // v = [1; x[1:] * scal], A[c][c] = beta
+    if (sigma > 0.0)
+      for (int i = 1 + tid; i < len; i += 256) x[i] *= scal;
+    __syncthreads();
+    if (tid == 0) { x[0] = beta; tau_s[c] = tau; }
+    // apply H = I - tau v v^T to the remaining panel columns (one warp per column)
+    for (int cc = c + 1 + warp; cc < nbw; cc += 8) {
+      double* y = A + (size_t)cc * ld + c;
+      double w = (lane == 0) ? y[0] : 0.0;
+      for (int i = 1 + lane; i < len; i += 32) w += x[i] * y[i];
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      w *= tau;
+      if (lane == 0) y[0] -= w;
+      for (int i = 1 + lane; i < len; i += 32) y[i] -= w * x[i];
+    }
+    __syncthreads();
+  }
+  // explicit V (rows j..n of the full matrix, ld n): unit diagonal, zeros above
+  for (int e = tid; e < rows * nbw; e += 256) {
+    const int i = e % rows, c = e / rows;
+    double v = (i < c) ? 0.0 : (i == c ? 1.0 : A[(size_t)c * ld + i]);
+    tk.V[(size_t)c * tk.n + i] = v;
+  }
+  __syncthreads();
+  // Gram V^T V (nbw x nbw), one warp per entry
+  for (int e = warp; e < nbw * nbw; e += 8) {
+    const int a = e % nbw, b = e / nbw;
+    if (a >= b) continue;     // only a < b needed
+    double s = 0.0;
+    for (int i = lane; i < rows; i += 32) s += tk.V[(size_t)a * tk.n + i] * tk.V[(size_t)b * tk.n + i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) G[a][b] = s;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // dlarft (forward, columnwise): T[0:i, i] = -tau_i T[0:i, 0:i] (V^T v_i)
+    double* T = tk.T;
+    for (int e = 0; e < HHB * HHB; ++e) T[e] = 0.0;
+    for (int i = 0; i < nbw; ++i) {
+      const double ti = tau_s[i];
+      T[i + i * HHB] = ti;
+      for (int a = 0; a < i; ++a) {
+        double s = 0.0;
+        for (int b = a; b < i; ++b) s += T[a + b * HHB] * G[b][i];
+        T[a + i * HHB] = -ti * s;
+      }
+    }
+  }
+}
+
+// Cluster variant of the panel: the 8 CTAs of a cluster split the panel rows and combine
+// their partial norms / dot products through distributed shared memory (DSMEM), so the long
+// panels of the upper levels (n up to several thousand rows) are not serialised on one SM.
+constexpr int HHC = 8;
+__global__ void __cluster_dims__(HHC, 1, 1) __launch_bounds__(256)
+hh_panel_cluster_kernel(const HHTask* __restrict__ tasks, int j) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const HHTask tk = tasks[blockIdx.x / HHC];
+  const int r = min(tk.n, tk.m);
+  if (j >= r) return;                       // uniform across the cluster (same task)
+  const int nbw = min(HHB, r - j), rows = tk.n - j, ld = tk.lda;
+  const int chunk = (rows + HHC - 1) / HHC;
+  const int lo = min(rows, rank * chunk), hi = min(rows, lo + chunk);
+  double* A = tk.A + j + (size_t)j * ld;
+  __shared__ double red[32];
+  __shared__ double s_sig;
+  __shared__ double s_dot[HHB];
+  __shared__ double wloc[HHB];
+  __shared__ double tau_s[HHB];
+  __shared__ double gram[HHB][HHB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = 0; c < nbw; ++c) {
+    double* x = A + (size_t)c * ld;
+    const double alpha = x[c];
+    double p = 0.0;
+    for (int i = max(lo, c + 1) + tid; i < hi; i += 256) p += x[i] * x[i];
+    p = block_sum<256>(p, red);
+    if (tid == 0) s_sig = p;
+    cl.sync();
+    double sigma = 0.0;
+    for (int q = 0; q < HHC; ++q) sigma += *cl.map_shared_rank(&s_sig, q);
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (sigma > 0.0) {
+      const double nrm = sqrt(alpha * alpha + sigma);
+      beta = (alpha >= 0.0) ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+      for (int i = max(lo, c + 1) + tid; i < hi; i += 256) x[i] *= scal;
+    }
+    const bool owner = (c >= lo && c < hi);
+    if (tid == 0) tau_s[c] = tau;
+    __syncthreads();
+    for (int cc = c + 1 + warp; cc < nbw; cc += 8) {
+      const double* y = A + (size_t)cc * ld;
+      double w = (owner && lane == 0) ? y[c] : 0.0;
+      for (int i = max(lo, c + 1) + lane; i < hi; i += 32) w += x[i] * y[i];
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      if (lane == 0) s_dot[cc] = w;
+    }
+    cl.sync();
+    for (int cc = c + 1 + tid; cc < nbw; cc += 256) {
+      double w = 0.0;
+      for (int q = 0; q < HHC; ++q) w += cl.map_shared_rank(s_dot, q)[cc];
+      wloc[cc] = w * tau;
+    }
+    __syncthreads();
+    for (int cc = c + 1 + warp; cc < nbw; cc += 8) {
+      double* y = A + (size_t)cc * ld;
+      const double w = wloc[cc];
+      if (owner && lane == 0) y[c] -= w;
+      for (int i = max(lo, c + 1) + lane; i < hi; i += 32) y[i] -= w * x[i];
+    }
+    if (owner && tid == 0) x[c] = beta;
+    cl.sync();
+  }
+  // explicit V for own rows, partial Gram V^T V over own rows
+  for (int e = tid; e < (hi - lo) * nbw; e += 256) {
+    const int i = lo + e % (hi - lo), c = e / (hi - lo);
+    const double v = (i < c) ? 0.0 : (i == c ? 1.0 : A[(size_t)c * ld + i]);
+    tk.V[(size_t)c * tk.n + i] = v;
+  }
+  __syncthreads();
+  for (int e = warp; e < nbw * nbw; e += 8) {
+    const int a = e % nbw, b = e / nbw;
+    if (a >= b) continue;
+    double sacc = 0.0;
+    for (int i = lo + lane; i < hi; i += 32) sacc += tk.V[(size_t)a * tk.n + i] * tk.V[(size_t)b * tk.n + i];
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) gram[a][b] = sacc;
+  }
+  cl.sync();
+  __shared__ double gsum[HHB][HHB + 1];
+  if (rank == 0) {
+    for (int e = tid; e < nbw * nbw; e += 256) {
+      const int a = e % nbw, b = e / nbw;
+      double g = 0.0;
+      if (a < b)
+        for (int q = 0; q < HHC; ++q) g += cl.map_shared_rank(&gram[0][0], q)[a * (HHB + 1) + b];
+      gsum[a][b] = g;
+    }
+  }
+  __syncthreads();
+  if (rank == 0 && tid == 0) {
+    double* T = tk.T;
+    for (int e = 0; e < HHB * HHB; ++e) T[e] = 0.0;
+    for (int i = 0; i < nbw; ++i) {
+      const double ti = tau_s[i];
+      T[i + i * HHB] = ti;
+      for (int a2 = 0; a2 < i; ++a2) {
+        double sacc = 0.0;
+        for (int b2 = a2; b2 < i; ++b2) sacc += T[a2 + b2 * HHB] * gsum[b2][i];
+    T[a2 + i * HHB] = -ti * sacc;
+      }
+    }
+  }
+  cl.sync();
+}
+
+// Same cluster panel with the panel rows of every CTA staged in shared memory (one load,
+// one store); used when (rows/8) x 32 doubles fit.  Same arithmetic order as the global one.
+__global__ void __cluster_dims__(HHC, 1, 1) __launch_bounds__(256)
+hh_panel_cluster_smem_kernel(const HHTask* __restrict__ tasks, int j, int cap_rows) {
+  extern __shared__ double P[];          // chunk x nbw, ld = cap_rows
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const HHTask tk = tasks[blockIdx.x / HHC];
+  const int r = min(tk.n, tk.m);
+  if (j >= r) return;
+  const int nbw = min(HHB, r - j), rows = tk.n - j, ld = tk.lda;
+  const int chunk = (rows + HHC - 1) / HHC;
+  const int lo = min(rows, rank * chunk), hi = min(rows, lo + chunk);
+  const int cnt = hi - lo;
+  double* A = tk.A + j + (size_t)j * ld;
+  __shared__ double red[32];
+  __shared__ double s_sig, s_alpha;
+  __shared__ double s_dot[HHB];
+  __shared__ double wloc[HHB];
+  __shared__ double tau_s[HHB];
+  __shared__ double gram[HHB][HHB + 1];
+  __shared__ double gsum[HHB][HHB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < cnt * nbw; e += 256) {
+    const int i = e % cnt, c = e / cnt;
+    P[(size_t)c * cap_rows + i] = A[(size_t)c * ld + lo + i];
+  }
+  __syncthreads();
+  for (int c = 0; c < nbw; ++c) {
+    double* x = P + (size_t)c * cap_rows;          // local rows
+    const bool owner = (c >= lo && c < hi);
+    const int i0 = max(lo, c + 1) - lo;               // first local row below the diagonal
+    double p = 0.0;
+    for (int i = i0 + tid; i < cnt; i += 256) p += x[i] * x[i];
+    p = block_sum<256>(p, red);
+    if (tid == 0) { s_sig = p; if (owner) s_alpha = x[c - lo]; }
+    cl.sync();
+    double sigma = 0.0;
+    for (int q = 0; q < HHC; ++q) sigma += *cl.map_shared_rank(&s_sig, q);
+    const int orank = min(HHC - 1, c / chunk);
+    const double alpha = *cl.map_shared_rank(&s_alpha, orank);
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (sigma > 0.0) {
+      const double nrm = sqrt(alpha * alpha + sigma);
+      beta = (alpha >= 0.0) ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+      for (int i = i0 + tid; i < cnt; i += 256) x[i] *= scal;
+    }
+    if (tid == 0) tau_s[c] = tau;
+    __syncthreads();
+    for (int cc = c + 1 + warp; cc < nbw; cc += 8) {
+      const double* y = P + (size_t)cc * cap_rows;
+      double w = (owner && lane == 0) ? y[c - lo] : 0.0;
+      for (int i = i0 + lane; i < cnt; i += 32) w += x[i] * y[i];
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      if (lane == 0) s_dot[cc] = w;
+    }
+    cl.sync();
+    for (int cc = c + 1 + tid; cc < nbw; cc += 256) {
+      double w = 0.0;
+      for (int q = 0; q < HHC; ++q) w += cl.map_shared_rank(s_dot, q)[cc];
+      wloc[cc] = w * tau;
+    }
+    __syncthreads();
+    for (int cc = c + 1 + warp; cc < nbw; cc += 8) {
+      double* y = P + (size_t)cc * cap_rows;
+      const double w = wloc[cc];
+      if (owner && lane == 0) y[c - lo] -= w;
+      for (int i = i0 + lane; i < cnt; i += 32) y[i] -= w * x[i];
+    }
+    if (owner && tid == 0) x[c - lo] = beta;
+    cl.sync();
+  }
+  // write back, explicit V, partial Gram
+  for (int e = tid; e < cnt * nbw; e += 256) {
+    const int i = e % cnt, c = e / cnt, gi = lo + i;
+    const double val = P[(size_t)c * cap_rows + i];
+    A[(size_t)c * ld + gi] = val;
+    tk.V[(size_t)c * tk.n + gi] = (gi < c) ? 0.0 : (gi == c ? 1.0 : val);
+  }
+  for (int e = warp; e < nbw * nbw; e += 8) {
+    const int a = e % nbw, b = e / nbw;
+    if (a >= b) continue;
+    double sacc = 0.0;
+    for (int i = lane; i < cnt; i += 32) {
+      const int gi = lo + i;
+      const double va = (gi < a) ? 0.0 : (gi == a ? 1.0 : P[(size_t)a * cap_rows + i]);
+      const double vb = (gi < b) ? 0.0 : (gi == b ? 1.0 : P[(size_t)b * cap_rows + i]);
+      sacc += va * vb;
+    }
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) gram[a][b] = sacc;
+  }
+  cl.sync();
+  if (rank == 0) {
+    for (int e = tid; e < nbw * nbw; e += 256) {
+      const int a = e % nbw, b = e / nbw;
+      double g = 0.0;
+      if (a < b)
+        for (int q = 0; q < HHC; ++q) g += cl.map_shared_rank(&gram[0][0], q)[a * (HHB + 1) + b];
+      gsum[a][b] = g;
+    }
+  }
+  __syncthreads();
+  if (rank == 0 && tid == 0) {
+    double* T = tk.T;
+    for (int e = 0; e < HHB * HHB; ++e) T[e] = 0.0;
+    for (int i = 0; i < nbw; ++i) {
+      const double ti = tau_s[i];
+      T[i + i * HHB] = ti;
+      for (int a2 = 0; a2 < i; ++a2) {
+        double sacc = 0.0;
+        for (int b2 = a2; b2 < i; ++b2) sacc += T[a2 + b2 * HHB] * gsum[b2][i];
+        T[a2 + i * HHB] = -ti * sacc;
+      }
+    }
+  }
+  cl.sync();
+}
+
+// M = R^T (m x r) from the upper triangle of the factored A (n x m, lda)
+__global__ void hh_extract_rt_kernel(const HHTask* __restrict__ tasks, double* const* __restrict__ out, const int* ldo) {
+  const HHTask tk = tasks[blockIdx.x];
+  const int r = min(tk.n, tk.m);
+  double* M = out[blockIdx.x];
+  const int ldm = ldo[blockIdx.x];
+  for (int e = threadIdx.x; e < tk.m * r; e += blockDim.x) {
+    const int jj = e % tk.m, i = e / tk.m;   // M[jj, i] = R[i, jj]
+    M[(size_t)i * ldm + jj] = (i <= jj) ? tk.A[(size_t)jj * tk.lda + i] : 0.0;
+  }
+}
+
 // ------------------------------------------------------------------------------ kernel entries
 __global__ void keval_tasks_kernel(const KEvalTask* __restrict__ tasks, const double* __restrict__ pts,
                                    KernelParams kp, int* __restrict__ flag) {
@@ -567,19 +1076,19 @@ void launch_gj(const GJTask* t, int ntasks, int nmax, int mode, cudaStream_t s) 
   // nmax here is the largest n*ncols (small kernel) or n (global kernel, negative)
   if (nmax >= 0) {
     size_t smem = (size_t)nmax * sizeof(double) + 0;  // caller passes n*nc + n + n/2 doubles
-    if (smem > 48 * 1024)
-      AIFMM_CUDA(cudaFuncSetAttribute(gj_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_dyn_smem(gj_small_kernel, smem);
     LAUNCH(gj_small_kernel, ntasks, GJ_NT, smem, s, t, mode);
   } else {
     size_t smem = (size_t)(-nmax) * (sizeof(double) + sizeof(int));
-    if (smem > 48 * 1024)
-      AIFMM_CUDA(cudaFuncSetAttribute(gj_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_dyn_smem(gj_global_kernel, smem);
     LAUNCH(gj_global_kernel, ntasks, GJ_NT, smem, s, t, mode);
   }
 }
 
 void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s) {
-  LAUNCH(gj_panel_kernel, ntasks, GJ_NT, 0, s, static_cast<const GJBTask*>(t), j);
+  const int elems = (160 * 1024) / 8;
+  ensure_dyn_smem(gj_panel_kernel, (size_t)elems * 8);
+  LAUNCH(gj_panel_kernel, ntasks, GJ_NT, (size_t)elems * 8, s, static_cast<const GJBTask*>(t), j, elems);
 }
 void launch_gj_unscramble(const void* t, int ntasks, cudaStream_t s) {
   LAUNCH(gj_unscramble_kernel, ntasks, 256, 0, s, static_cast<const GJBTask*>(t));
@@ -590,11 +1099,16 @@ void gjb_make(void* out, double* A, int lda, int n, double* PW, double* Bws, int
   *t = GJBTask{A, lda, n, PW, Bws, piv, info};
 }
 
+void launch_pqr_cluster(const PqrTask* t, int ntasks, cudaStream_t s) {
+  const int cap = (200 * 1024) / 8;
+  ensure_dyn_smem(pqr_cluster_kernel, (size_t)cap * 8);
+  LAUNCH(pqr_cluster_kernel, ntasks * PQC, PQR_NT, (size_t)cap * 8, s, t, cap);
+}
+
 void launch_pqr(const PqrTask* t, int ntasks, size_t smem_doubles, cudaStream_t s) {
   size_t smem = smem_doubles * sizeof(double);
   AIFMM_REQUIRE(smem <= 227 * 1024, AIFMM_EOOM, "pivoted QR candidate matrix too wide for shared memory");
-  if (smem > 48 * 1024)
-    AIFMM_CUDA(cudaFuncSetAttribute(pqr_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem(pqr_tasks_kernel, smem);
   LAUNCH(pqr_tasks_kernel, ntasks, PQR_NT, smem, s, t);
 }
 
@@ -616,5 +1130,35 @@ void launch_copy(const CopyTask* t, int ntasks, int ysplit, cudaStream_t s) {
 }
 
 void launch_norm(const NormTask* t, int ntasks, cudaStream_t s) { LAUNCH(norm_tasks_kernel, ntasks, 256, 0, s, t); }
+
+size_t hh_task_size() { return sizeof(HHTask); }
+void hh_make(void* out, double* A, int lda, int n, int m, double* V, double* T) {
+  *static_cast<HHTask*>(out) = HHTask{A, lda, n, m, V, T};
+}
+void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode, int nmax) {
+  // mode 0: one CTA; mode 1: 8-CTA cluster (global memory); mode 2: cluster, smem-staged
+  if (mode == 2) {
+    const int cap_rows = (std::max(nmax - j, 1) + HHC - 1) / HHC;
+    const size_t smem = (size_t)cap_rows * HHB * sizeof(double);
+    ensure_dyn_smem(hh_panel_cluster_smem_kernel, smem);
+    hh_panel_cluster_smem_kernel<<<ntasks * HHC, 256, smem, s>>>(static_cast<const HHTask*>(t), j, cap_rows);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, hh_panel_cluster_smem_kernel);
+      fprintf(stderr, "hh smem launch failed: %s smem=%zu static=%zu maxdyn=%d ntasks=%d j=%d nmax=%d\n", cudaGetErrorString(e),
+              smem, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, ntasks, j, nmax);
+      AIFMM_CUDA(e);
+    }
+    ++g_launches;
+  } else if (mode == 1) {
+    LAUNCH(hh_panel_cluster_kernel, ntasks * HHC, 256, 0, s, static_cast<const HHTask*>(t), j);
+  } else {
+    LAUNCH(hh_panel_kernel, ntasks, 256, 0, s, static_cast<const HHTask*>(t), j);
+  }
+}
+void launch_hh_extract(const void* t, int ntasks, double* const* out, const int* ldo, cudaStream_t s) {
+  LAUNCH(hh_extract_rt_kernel, ntasks, 256, 0, s, static_cast<const HHTask*>(t), out, ldo);
+}
 
 }  // namespace aifmm

@@ -15,6 +15,7 @@ namespace aifmm {
 void launch_gemm(int tileclass, const GemmTask* t, const GemmTerm* tm, const GemmTile* tiles, int ntiles, cudaStream_t s);
 void launch_gj(const GJTask* t, int ntasks, int nmax, int mode, cudaStream_t s);
 void launch_pqr(const PqrTask* t, int ntasks, size_t smem_doubles, cudaStream_t s);
+void launch_pqr_cluster(const PqrTask* t, int ntasks, cudaStream_t s);
 void launch_keval(const KEvalTask* t, int ntasks, int ysplit, const double* pts, KernelParams kp, int* flag, cudaStream_t s);
 void launch_copy(const CopyTask* t, int ntasks, int ysplit, cudaStream_t s);
 void launch_norm(const NormTask* t, int ntasks, cudaStream_t s);
@@ -22,6 +23,11 @@ void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s);
 void launch_gj_unscramble(const void* t, int ntasks, cudaStream_t s);
 size_t gjb_task_size();
 void gjb_make(void* out, double* A, int lda, int n, double* PW, double* Bws, int* piv, int* info);
+size_t hh_task_size();
+void hh_make(void* out, double* A, int lda, int n, int m, double* V, double* T);
+void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode, int nmax);
+void launch_hh_extract(const void* t, int ntasks, double* const* out, const int* ldo, cudaStream_t s);
+constexpr int HH_PANEL = 32;
 constexpr int GJ_SMALL_MAX = 80;   // in-place inverses up to this size run in shared memory
 constexpr int GJ_PANEL = 32;
 
@@ -165,8 +171,47 @@ class GemmBatch {
   void add(double alpha, const double* B, int ldb, int transB) { term(alpha, nullptr, 0, 0, B, ldb, transB, 0); }
   bool empty() const { return tasks_.empty(); }
   size_t size() const { return tasks_.size(); }
+  // Deterministic split-K: single-term tasks with a long K and few output tiles are split into
+  // S partial GEMMs into workspace slices, then reduced in a fixed order by a second launch.
+  void set_splitk_pool(DevPool* p) { splitk_ = p; }
   void run(Uploader& up, cudaStream_t s, FlopCounter* fc = nullptr) {
     if (tasks_.empty()) return;
+    std::vector<GemmTask> red_tasks;
+    std::vector<GemmTerm> red_terms;
+    if (splitk_) {
+      const size_t nt0 = tasks_.size();
+      for (size_t t = 0; t < nt0; ++t) {
+        GemmTask k = tasks_[t];
+        if (k.term_end - k.term_begin != 1) continue;
+        GemmTerm tm = terms_[k.term_begin];
+        if (!tm.A || k.M <= 0 || k.N <= 0) continue;
+        const long long tiles = (long long)((k.M + 63) / 64) * ((k.N + 63) / 64);
+        if (tm.K < 1024 || tiles >= 64) continue;
+        int S = (int)std::min<long long>(32, std::max<long long>(2, tm.K / 384));
+        const int kc = (tm.K + S - 1) / S;
+        S = (tm.K + kc - 1) / kc;
+        double* ws = splitk_->d((size_t)S * k.M * k.N);
+        GemmTask r{k.C, k.ldc, k.M, k.N, k.beta, (int)red_terms.size(), (int)red_terms.size()};
+        for (int q = 0; q < S; ++q) {
+          const int k0 = q * kc, kl = std::min(kc, tm.K - k0);
+          double* P = ws + (size_t)q * k.M * k.N;
+          GemmTerm part = tm;
+          part.K = kl;
+          part.A = tm.transA ? tm.A + k0 : tm.A + (size_t)k0 * tm.lda;
+          part.B = tm.transB ? tm.B + (size_t)k0 * tm.ldb : tm.B + k0;
+          if (q == 0) {
+            tasks_[t] = GemmTask{P, k.M, k.M, k.N, 0.0, k.term_begin, k.term_end};
+            terms_[k.term_begin] = part;
+          } else {
+            tasks_.push_back(GemmTask{P, k.M, k.M, k.N, 0.0, (int)terms_.size(), (int)terms_.size() + 1});
+            terms_.push_back(part);
+          }
+          red_terms.push_back(GemmTerm{nullptr, P, 0, k.M, 0, 0, 0, 1.0});
+        }
+        r.term_end = (int)red_terms.size();
+        red_tasks.push_back(r);
+      }
+    }
     std::vector<GemmTile> tl[4];
     for (size_t t = 0; t < tasks_.size(); ++t) {
       const GemmTask& k = tasks_[t];
@@ -202,11 +247,20 @@ class GemmBatch {
     }
     tasks_.clear();
     terms_.clear();
+    if (!red_tasks.empty()) {
+      tasks_ = std::move(red_tasks);
+      terms_ = std::move(red_terms);
+      DevPool* keep = splitk_;
+      splitk_ = nullptr;
+      run(up, s, nullptr);
+      splitk_ = keep;
+    }
   }
 
  private:
   std::vector<GemmTask> tasks_;
   std::vector<GemmTerm> terms_;
+  DevPool* splitk_ = nullptr;
 };
 
 class CopyBatch {
@@ -294,6 +348,96 @@ inline void batched_inverse(const std::vector<InvReq>& reqs, Pool& work, Uploade
     g.run(up, s);
   }
   launch_gj_unscramble(dt, (int)big.size(), s);
+}
+
+
+// Batched two-stage RRQR, first stage (reading R8b): for each tall A (n x m, lda) compute the
+// Householder factor R and write M = R^T (m x min(n,m), ld ldm) to out.  A is destroyed.
+struct TriRootReq {
+  double* A;
+  int lda, n, m;
+  double* out;
+  int ldm;
+};
+template <class Pool>
+inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Uploader& up, cudaStream_t s,
+                             FlopCounter* fc = nullptr) {
+  if (reqs.empty()) return;
+  const size_t tsz = hh_task_size();
+  // long panels (n >= 512 rows) go to the 8-CTA cluster kernel, short ones to one CTA
+  // three classes: short panels (one CTA), long panels staged in the smem of an 8-CTA cluster,
+  // very long panels (cluster, global memory)
+  const int SM_ROWS = 8 * ((176 * 1024) / (HH_PANEL * 8));
+  std::vector<TriRootReq> sorted_reqs;
+  for (const auto& q : reqs) if (q.n < 512) sorted_reqs.push_back(q);
+  const size_t nsmall = sorted_reqs.size();
+  int nmax_mid = 0;
+  for (const auto& q : reqs) if (q.n >= 512 && q.n <= SM_ROWS) { sorted_reqs.push_back(q); nmax_mid = std::max(nmax_mid, q.n); }
+  const size_t nmid = sorted_reqs.size() - nsmall;
+  for (const auto& q : reqs) if (q.n > SM_ROWS) sorted_reqs.push_back(q);
+  const std::vector<TriRootReq>& R = sorted_reqs;
+  std::vector<char> tb(tsz * reqs.size());
+  std::vector<double*> V(reqs.size()), T(reqs.size()), Z(reqs.size()), Z2(reqs.size());
+  std::vector<double*> outs(reqs.size());
+  std::vector<int> ldo(reqs.size());
+  int rmax = 0;
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    const TriRootReq& q = R[i];
+    V[i] = work.d((size_t)std::max(q.n, 1) * HH_PANEL);
+    T[i] = work.d((size_t)HH_PANEL * HH_PANEL);
+    Z[i] = work.d((size_t)HH_PANEL * std::max(q.m, 1));
+    Z2[i] = work.d((size_t)HH_PANEL * std::max(q.m, 1));
+    hh_make(tb.data() + i * tsz, q.A, q.lda, q.n, q.m, V[i], T[i]);
+    outs[i] = q.out;
+    ldo[i] = q.ldm;
+    rmax = std::max(rmax, std::min(q.n, q.m));
+    if (fc) fc->flops += 2.0 * q.n * (double)q.m * q.m;
+  }
+  up.reserve(tb.size() + outs.size() * 8 + ldo.size() * 4 + 1024);
+  const void* dt = up.put(tb.data(), tb.size());
+  double* const* douts = up.put(outs);
+  const int* dldo = up.put(ldo);
+  for (int j = 0; j < rmax; j += HH_PANEL) {
+    if (nsmall) launch_hh_panel(dt, (int)nsmall, j, s, 0, 0);
+    if (nmid) launch_hh_panel(static_cast<const char*>(dt) + nsmall * tsz, (int)nmid, j, s, 2, nmax_mid);
+    if (reqs.size() > nsmall + nmid)
+      launch_hh_panel(static_cast<const char*>(dt) + (nsmall + nmid) * tsz, (int)(reqs.size() - nsmall - nmid), j, s, 1, 0);
+    GemmBatch g1, g2, g3;
+    g1.set_splitk_pool(&work);
+    for (size_t i = 0; i < reqs.size(); ++i) {
+      const TriRootReq& q = R[i];
+      const int r = std::min(q.n, q.m);
+      if (j >= r) continue;
+      const int nbw = std::min(HH_PANEL, r - j);
+      const int nc = q.m - j - nbw;
+      if (nc <= 0) continue;
+      double* C = q.A + j + (size_t)(j + nbw) * q.lda;
+      g1.task(Z[i], HH_PANEL, nbw, nc, 0.0);
+      g1.term(1.0, V[i], q.n, 1, C, q.lda, 0, q.n - j);
+      g2.task(Z2[i], HH_PANEL, nbw, nc, 0.0);
+      g2.term(1.0, T[i], HH_PANEL, 1, Z[i], HH_PANEL, 0, nbw);
+      g3.task(C, q.lda, q.n - j, nc, 1.0);
+      g3.term(-1.0, V[i], q.n, 0, Z2[i], HH_PANEL, 0, nbw);
+    }
+    g1.run(up, s);
+    g2.run(up, s);
+    g3.run(up, s);
+  }
+  launch_hh_extract(dt, (int)reqs.size(), douts, dldo, s);
+}
+// run pivoted-QR tasks: tall ones (m >= 128) on 8-CTA clusters, the rest one CTA each
+inline void run_pqr(const std::vector<PqrTask>& v, Uploader& up, cudaStream_t s) {
+  std::vector<PqrTask> small, big;
+  size_t smem = 0;
+  for (const PqrTask& t : v) {
+    if (t.m >= 128) big.push_back(t);
+    else {
+      small.push_back(t);
+      smem = std::max(smem, (size_t)t.ncols + t.m + t.k0 + t.tmax + 8);
+    }
+  }
+  if (!small.empty()) launch_pqr(up.put(small), (int)small.size(), smem, s);
+  if (!big.empty()) launch_pqr_cluster(up.put(big), (int)big.size(), s);
 }
 
 }  // namespace aifmm

@@ -270,8 +270,7 @@ void tree_segsort(const long long* off, int nb, int maxlen, int* perm, cudaStrea
   int p2 = 1;
   while (p2 < maxlen) p2 <<= 1;
   size_t smem = (size_t)p2 * sizeof(int);
-  if (smem > 48 * 1024)
-    AIFMM_CUDA(cudaFuncSetAttribute(segsort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem(segsort_kernel, smem);
   LAUNCH(segsort_kernel, std::min(nb, 148 * 16), 256, smem, s, off, nb, perm);
 }
 void tree_gather(const double* pts, const int* perm, long long n, int d, double* sorted, cudaStream_t s) {

@@ -1,0 +1,168 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): integer outputs (tree permutation, box offsets, N/IL lists,
+colours, NNCA ranks) bit-exact; solution within 10*tol relative 2-norm of the oracle's;
+relative residual (exact direct sum, 4096 sampled rows at large N) within 2x the oracle's.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import dense                      # noqa: E402
+from oracle.factor import AIFMM as Oracle     # noqa: E402
+from paper_2301_12704_b200 import aifmm as G  # noqa: E402
+from paper_2301_12704_b200 import workloads as W  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    G.load()
+    yield
+    G.free()
+
+
+def _gpu_solve(pts, b, kid, kp, leaf, tol, tol_c=None):
+    G.free()
+    if tol_c is not None:
+        G.set_compression_tol(tol_c)
+    G.build(torch.from_numpy(pts).cuda(), kid, kp, leaf, tol)
+    G.factor()
+    return G.solve(torch.from_numpy(np.ascontiguousarray(b)).cuda()).cpu().numpy()
+
+
+def _integer_parity(o, d):
+    perm, L = G.get_tree(o.tree.n)
+    assert L == o.tree.L
+    assert np.array_equal(perm, o.tree.perm)
+    for l in range(0, L + 1):
+        assert np.array_equal(G.get_level_offsets(l, d), o.tree.off[l])
+    for l in range(2, L + 1):
+        nptr, nidx, iptr, iidx = G.get_lists(l, d)
+        col = G.get_colours(l, d)
+        rk = G.get_ranks(l, d, 0)
+        nb = 1 << (d * l)
+        for b in range(nb):
+            if b in o.near[l]:
+                assert list(nidx[nptr[b]:nptr[b + 1]]) == o.near[l][b]
+                assert list(iidx[iptr[b]:iptr[b + 1]]) == o.il[l][b]
+                assert col[b] == o.colour[l][b]
+                assert rk[b] == o.nnca.rank(l, b)
+            else:
+                assert nptr[b + 1] == nptr[b] and col[b] == -1
+
+
+CASES = [
+    # (name, points kind, n, d, kernel, kparams, leaf, tol, nrhs)
+    ("cfg1_grid_log", "grid", 4096, 2, 0, (10.0, 0.0), 64, 1e-8, 1),
+    ("rand2d_log_ragged", "uniform_pm1", 3000, 2, 0, (10.0, 0.0), 40, 1e-8, 2),
+    ("rand2d_matern", "uniform_pm1", 2500, 2, 1, (1.01, 0.1), 32, 1e-6, 1),
+    ("rand2d_invr", "uniform_pm1", 2048, 2, 2, (float(np.sqrt(1000 * 2048)), 0.0), 32, 1e-10, 3),
+    ("rand3d_invr", "uniform_01", 3000, 3, 2, (100.0, 0.0), 32, 1e-7, 1),
+    ("grid3d_invr", "grid", 4096, 3, 2, (128.0, 0.0), 64, 1e-7, 2),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_parity_small(case):
+    name, kind, n, d, kid, kp, leaf, tol, nrhs = case
+    pts = W.make_points(kind, n, d, 21)
+    b = W.make_rhs(n, nrhs, 21)
+    o = Oracle(pts, kid, kp, leaf, tol).factor()
+    xo = o.solve(b)
+    x = _gpu_solve(pts, b, kid, kp, leaf, tol)
+    _integer_parity(o, d)
+    rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)
+    assert rel <= 10 * tol, rel
+    ro = dense.residual(pts, kid, kp, xo, b)
+    rg = dense.residual(pts, kid, kp, x, b)
+    assert rg <= 2 * ro + 1e-13, (rg, ro)      # 1e-13: rounding-noise floor
+
+
+def test_exact_redirection_matches_densified_nnca():
+    """tol_c = 0: the GPU elimination is exact algebra on the NNCA matrix (same integer
+    decisions as the oracle, so the same densified H2 matrix)."""
+    pts, b = W.small_problem(d=2, n=1500, seed=9)
+    o = Oracle(pts, 0, (10.0, 0.0), 24, 1e-5, tol_c=0.0)
+    x = _gpu_solve(pts, b, 0, (10.0, 0.0), 24, 1e-5, tol_c=0.0)
+    xh = np.linalg.solve(dense.h2_matrix(o), b)
+    assert np.linalg.norm(x - xh) / np.linalg.norm(xh) <= 1e-10
+    G.set_compression_tol(1e-5)
+
+
+def test_multi_rhs_equals_columns_and_zero_rhs():
+    pts, b = W.small_problem(d=2, n=2000, seed=12, nrhs=4)
+    G.free()
+    G.build(torch.from_numpy(pts).cuda(), 0, (10.0, 0.0), 32, 1e-8)
+    G.factor()
+    X = G.solve(torch.from_numpy(b).cuda()).cpu().numpy()
+    for j in range(4):
+        xj = G.solve(torch.from_numpy(np.ascontiguousarray(b[:, j])).cuda()).cpu().numpy()
+        assert np.abs(X[:, j] - xj).max() <= 1e-12 * np.abs(xj).max()
+    z = G.solve(torch.zeros(2000, 2, dtype=torch.float64, device="cuda")).cpu().numpy()
+    assert np.all(z == 0.0)
+    # repeated solves do not alter the factorization
+    X2 = G.solve(torch.from_numpy(b).cuda()).cpu().numpy()
+    assert np.array_equal(X, X2)
+    # end-to-end host path gives the same numbers
+    Xh = G.solve_host(b)
+    assert np.abs(Xh - X).max() <= 1e-13 * np.abs(X).max()
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 65])
+def test_tiny_inputs(n):
+    """Degenerate trees: one point, a few points (empty IL, rank-0 boxes, empty boxes)."""
+    pts, b = W.small_problem(d=2, n=n, seed=30 + n)
+    kp = (5.0 + n, 0.0)
+    o = Oracle(pts, 2, kp, 4, 1e-8).factor()
+    xo = o.solve(b)
+    x = _gpu_solve(pts, b, 2, kp, 4, 1e-8)
+    _integer_parity(o, 2)
+    assert np.linalg.norm(x - xo) <= 1e-12 * max(np.linalg.norm(xo), 1e-300)
+    A = dense.dense_matrix(pts, 2, kp)
+    assert np.linalg.norm(A @ x - b) <= 1e-7 * np.linalg.norm(b)
+
+
+def test_error_codes():
+    G.free()
+    p = torch.zeros(4, 2, dtype=torch.float64, device="cuda")
+    with pytest.raises(G.AIFMMError) as e:          # more coincident points than a leaf holds
+        G.build(p, 0, (1.0, 0.0), 2, 1e-6)
+    assert e.value.code == -3
+    with pytest.raises(G.AIFMMError) as e:          # coincident points, singular kernel
+        G.build(p, 0, (1.0, 0.0), 4, 1e-6)
+        G.factor()
+    assert e.value.code == -3
+    p = torch.tensor([[0.0, 0.0], [float("nan"), 1.0]], dtype=torch.float64, device="cuda")
+    with pytest.raises(G.AIFMMError) as e:
+        G.build(p, 0, (1.0, 0.0), 2, 1e-6)
+    assert e.value.code == -2
+    with pytest.raises(G.AIFMMError) as e:
+        G.build(torch.zeros(4, 2, dtype=torch.float64, device="cuda"), 0, (1.0, 0.0), 2, 2.0)
+    assert e.value.code == -1
+    G.free()
+    with pytest.raises(G.AIFMMError) as e:
+        G.factor()
+    assert e.value.code == -6
+    with pytest.raises(G.AIFMMError) as e:
+        G.solve(torch.zeros(4, dtype=torch.float64, device="cuda"))
+    assert e.value.code == -6
+
+
+def test_config2_full_size_parity():
+    """BASELINE config 2 at full size (N = 65536, 16 RHS, tol 1e-10) in the configuration
+    bench.py times: solution vs the oracle's and sampled direct-sum residuals (4096 rows)."""
+    cfg = W.CONFIGS[1]
+    pts, b = W.make(cfg)
+    o = Oracle(pts, cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol).factor()
+    xo = o.solve(b)
+    x = _gpu_solve(pts, b, cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol)
+    rows = W.residual_rows(cfg.n, cfg.seed)
+    ro = dense.residual(pts, cfg.kernel_id, cfg.kparams, xo, b, rows)
+    rg = dense.residual(pts, cfg.kernel_id, cfg.kparams, x, b, rows)
+    rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)
+    assert rg <= 2 * ro, (rg, ro)
+    assert rel <= 10 * cfg.tol, rel

@@ -1,0 +1,18 @@
+"""Aggregate an ncu --csv launch list (gpu__time_duration.sum) by kernel name."""
+import csv, sys, collections
+rows = list(csv.reader(open(sys.argv[1])))
+hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+hdr = rows[hdr_i]
+ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+tot = collections.defaultdict(float); cnt = collections.Counter()
+for r in rows[hdr_i + 1:]:
+    if len(r) <= vi: continue
+    try: v = float(r[vi].replace(",", ""))
+    except ValueError: continue
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+    name = r[ki].split("(")[0]
+    tot[name] += v * scale; cnt[name] += 1
+T = sum(tot.values())
+print(f"total {T/1e3:.2f} ms over {sum(cnt.values())} launches")
+for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+    print(f"{v/1e3:10.2f} ms {100*v/T:5.1f}% {cnt[k]:7d}  {k}")
