@@ -159,28 +159,7 @@ struct Ctx {
   }
 };
 
-// Optional phase profile (AIFMM_PROFILE=1): synchronises at phase boundaries and prints a
-// breakdown to stderr at the end of factor / solve.  Off by default (no extra syncs).
-struct Prof {
-  bool on = false;
-  std::map<std::string, double> ms;
-  std::chrono::steady_clock::time_point t0;
-  cudaStream_t s = nullptr;
-  void begin(cudaStream_t st) { if (!on) return; s = st; cudaStreamSynchronize(s); t0 = std::chrono::steady_clock::now(); }
-  void end(const char* name) {
-    if (!on) return;
-    cudaStreamSynchronize(s);
-    ms[name] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  }
-  void dump(const char* title) {
-    if (!on) return;
-    fprintf(stderr, "[aifmm profile] %s:", title);
-    for (auto& kv : ms) fprintf(stderr, " %s=%.2fms", kv.first.c_str(), kv.second);
-    fprintf(stderr, "\n");
-    ms.clear();
-  }
-};
-static Prof g_prof;
+
 
 static Ctx* g_ctx = nullptr;
 static std::string g_err;
@@ -708,9 +687,16 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   int* dt = c.work.i(4 * na);
   CopyBatch cb;
   std::vector<NormTask> nt;
+  AIFMM_CUDA(cudaMemsetAsync(dt, 0, sizeof(int) * 4 * na, c.s));
+  std::vector<char> full(na, 0);
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
     const int m = f.m[b];
+    if (f.k[b] >= m) {            // basis already spans R^m: nothing to add (t = 0)
+      full[a] = 1;
+      su[a] = sv[a] = Side{nullptr, 0, nullptr, 0};
+      continue;
+    }
     int nu = 0;
     for (int q : part[b]) nu += live(f, q);
     su[a].n = sv[a].n = nu;
@@ -781,11 +767,12 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
     const int m = f.m[b], k = f.k[b];
+    if (full[a]) continue;
     pq.push_back(PqrTask{wu[a].W, f.U[b], m, m, m, wu[a].nc, k, 0, m - k, 0, dnorm + 2 * a, c.tol_c, dt + 4 * a, dt + 4 * a + 1});
     pq.push_back(PqrTask{wv[a].W, f.V[b], m, m, m, wv[a].nc, k, 0, m - k, 0, dnorm + 2 * a + 1, c.tol_c, dt + 4 * a + 2, dt + 4 * a + 3});
     smem = std::max(smem, (size_t)std::max(wu[a].nc, wv[a].nc) + m + m);
   }
-  run_pqr(pq, c.up, c.s);
+  if (!pq.empty()) run_pqr(pq, c.up, c.s);
   std::vector<int> th = d2h(c, dt, 4 * na);
   if (g_prof.on) { g_prof.end("cmp.pqrA"); g_prof.begin(c.s); }
   std::vector<int> tgt(na), hu(na), hv(na);
@@ -961,12 +948,20 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
   g.run(c.up, c.s, &c.fc_all);
   if (g_prof.on) { g_prof.end("elim.W"); g_prof.begin(c.s); }
   // 3. Schur updates, target-centric (deterministic ascending-i accumulation), + new blocks
-  std::map<std::pair<int, int>, std::vector<int>> targets;   // (p,q) -> list of a (index into cs)
+  // (p, q, a) triples sorted by target then by a (ascending eliminated box = fixed order)
+  struct Tg { long long key; int a; };
+  std::vector<Tg> tgs;
   for (size_t a = 0; a < cs.size(); ++a)
     for (int p : nbs[a])
-      for (int q : nbs[a]) targets[{p, q}].push_back((int)a);
-  for (auto& kv : targets) {
-    const int p = kv.first.first, q = kv.first.second;
+      for (int q : nbs[a]) tgs.push_back(Tg{f.key(p, q), (int)a});
+  std::sort(tgs.begin(), tgs.end(), [](const Tg& x, const Tg& y) { return x.key < y.key || (x.key == y.key && x.a < y.a); });
+  std::vector<int> grp_a;
+  for (size_t t0 = 0; t0 < tgs.size();) {
+    size_t t1 = t0;
+    grp_a.clear();
+    while (t1 < tgs.size() && tgs[t1].key == tgs[t0].key) grp_a.push_back(tgs[t1++].a);
+    const int p = (int)(tgs[t0].key / f.nb), q = (int)(tgs[t0].key % f.nb);
+    t0 = t1;
     const int M = live(f, p), N = live(f, q);
     if (!M || !N) continue;
     Blk T;
@@ -979,7 +974,7 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
       f.pending.insert({std::min(p, q), std::max(p, q)});
     }
     g.task(T.p, T.ld, M, N, 1.0);
-    for (int a : kv.second) {
+    for (int a : grp_a) {
       int i = cs[a];
       const int m = f.m[i], n = m + f.k[i];
       if (!m) continue;
@@ -1298,8 +1293,8 @@ int aifmm_build(const double* points, int64_t n, int d, int kernel_id, const dou
   AIFMM_REQUIRE(tol > 0.0 && tol < 1.0, AIFMM_EINVALID_ARG, "tol must lie in (0,1)");
   Ctx& c = ctx();
   auto t0 = std::chrono::steady_clock::now();
-  c.persist.release();
-  c.buildp.release();
+  c.persist.recycle();
+  c.buildp.recycle();
   c.work.reset();
   c.fl.clear();
   c.nn.clear();
@@ -1319,7 +1314,7 @@ int aifmm_build(const double* points, int64_t n, int d, int kernel_id, const dou
   build_nnca(c);
   g_prof.end("nnca");
   g_prof.dump("build");
-  c.buildp.release();
+  c.buildp.recycle();
   c.built = true;
   c.stats[AIFMM_STAT_LEVELS] = c.L;
   c.stats[AIFMM_STAT_BUILD_MS] = ms_since(t0);
@@ -1408,9 +1403,10 @@ void aifmm_free(void) {
   if (c.s) cudaStreamSynchronize(c.s);
   c.fl.clear();
   c.nn.clear();
-  c.persist.release();
-  c.work.release();
-  c.buildp.release();
+  // device memory stays cached in the pools (released at process exit or by a failing build)
+  c.persist.recycle();
+  c.work.reset();
+  c.buildp.recycle();
   c.built = c.factored = false;
   c.tol_c_user = -1;
 }

@@ -26,16 +26,29 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Batched variable-size GEMM on FP64 tensor cores.  One CTA = one BM x BN tile of one task;
+// the K loop runs over all terms of the task (deterministic order), operand tiles are staged
+// global -> shared by cp.async with a 2-stage double buffer, each warp owns a 32 x 32 sub-tile
+// (4 x 4 DMMA 8x8x4 fragments), alpha is applied to the A fragments in registers.
 template <int BM, int BN>
 __global__ void __launch_bounds__(BM * BN / 32)
 gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmTerm* __restrict__ terms,
                   const GemmTile* __restrict__ tiles) {
   constexpr int BK = 16;
-  constexpr int NT = BM * BN / 32;           // threads (one warp per 32x32 sub-tile)
+  constexpr int NT = BM * BN / 32;
   constexpr int LDS_A = BM + 4;              // (BM+4) % 16 == 4 -> conflict-free fragment loads
   constexpr int LDS_B = BN + 4;
-  __shared__ double sA[BK][LDS_A];
-  __shared__ double sB[BK][LDS_B];
+  __shared__ __align__(16) double sA[2][BK][LDS_A];
+  __shared__ __align__(16) double sB[2][BK][LDS_B];
 
   const GemmTile tile = tiles[blockIdx.x];
   const GemmTask tk = tasks[tile.task];
@@ -50,46 +63,66 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmTerm* __restrict
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int t = tk.term_begin; t < tk.term_end; ++t) {
+  // iteration state over (term, k0) K-tiles of the multiplicative terms
+  auto next_term = [&](int t) {
+    while (t < tk.term_end && terms[t].A == nullptr) ++t;
+    return t;
+  };
+  auto load = [&](int st, int t, int k0) {
     const GemmTerm tm = terms[t];
-    if (tm.A == nullptr) continue;  // additions are applied in the epilogue
-    const double alpha = tm.alpha;
-    for (int k0 = 0; k0 < tm.K; k0 += BK) {
-      // A tile: op(A)[m0:m0+BM, k0:k0+BK] -> sA[k][m]
-      for (int e = tid; e < BM * BK; e += NT) {
-        int mm, kk;
-        if (!tm.transA) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
-        int gm = m0 + mm, gk = k0 + kk;
-        double v = 0.0;
-        if (gm < tk.M && gk < tm.K)
-          v = tm.transA ? tm.A[(size_t)gm * tm.lda + gk] : tm.A[(size_t)gk * tm.lda + gm];
-        sA[kk][mm] = alpha * v;
-      }
-      // B tile: op(B)[k0:k0+BK, n0:n0+BN] -> sB[k][n]
-      for (int e = tid; e < BN * BK; e += NT) {
-        int nn, kk;
-        if (!tm.transB) { kk = e % BK; nn = e / BK; } else { nn = e % BN; kk = e / BN; }
-        int gn = n0 + nn, gk = k0 + kk;
-        double v = 0.0;
-        if (gn < tk.N && gk < tm.K)
-          v = tm.transB ? tm.B[(size_t)gk * tm.ldb + gn] : tm.B[(size_t)gn * tm.ldb + gk];
-        sB[kk][nn] = v;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < BK; kk += 4) {
-        double a[4], b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = sA[kk + (lane & 3)][wm + i * 8 + (lane >> 2)];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = sB[kk + (lane & 3)][wn + j * 8 + (lane >> 2)];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-      }
-      __syncthreads();
+    for (int e = tid; e < BM * BK; e += NT) {
+      int mm, kk;
+      if (!tm.transA) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
+      const int gm = m0 + mm, gk = k0 + kk;
+      const bool ok = gm < tk.M && gk < tm.K;
+      const double* src = ok ? (tm.transA ? tm.A + (size_t)gm * tm.lda + gk : tm.A + (size_t)gk * tm.lda + gm) : tm.A;
+      cp_async8(&sA[st][kk][mm], src, ok);
     }
+    for (int e = tid; e < BN * BK; e += NT) {
+      int nn, kk;
+      if (!tm.transB) { kk = e % BK; nn = e / BK; } else { nn = e % BN; kk = e / BN; }
+      const int gn = n0 + nn, gk = k0 + kk;
+      const bool ok = gn < tk.N && gk < tm.K;
+      const double* src = ok ? (tm.transB ? tm.B + (size_t)gk * tm.ldb + gn : tm.B + (size_t)gn * tm.ldb + gk) : tm.B;
+      cp_async8(&sB[st][kk][nn], src, ok);
+    }
+  };
+  int ct = next_term(tk.term_begin), ck = 0;
+  if (ct < tk.term_end) {
+    load(0, ct, 0);
+    cp_async_commit();
+  }
+  int st = 0;
+  while (ct < tk.term_end) {
+    // lookahead position
+    int nt = ct, nk = ck + BK;
+    if (nk >= terms[ct].K) { nt = next_term(ct + 1); nk = 0; }
+    const bool more = nt < tk.term_end;
+    if (more) {
+      load(st ^ 1, nt, nk);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double alpha = terms[ct].alpha;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = alpha * sA[st][kk + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = sB[st][kk + (lane & 3)][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+    st ^= 1;
+    ct = nt;
+    ck = nk;
   }
   // epilogue: C = beta*C + acc + sum(addition terms)
 #pragma unroll

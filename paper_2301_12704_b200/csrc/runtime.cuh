@@ -1,6 +1,9 @@
 // runtime.cuh — host-side runtime pieces of libaifmm: device pools, task upload arena, batch builders.
 #pragma once
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <string>
 #include <cstring>
 #include <map>
 #include <set>
@@ -30,6 +33,29 @@ void launch_hh_extract(const void* t, int ntasks, double* const* out, const int*
 constexpr int HH_PANEL = 32;
 constexpr int GJ_SMALL_MAX = 80;   // in-place inverses up to this size run in shared memory
 constexpr int GJ_PANEL = 32;
+
+// Optional phase profile (AIFMM_PROFILE=1): synchronises at phase boundaries and prints a
+// breakdown to stderr at the end of factor / solve.  Off by default (no extra syncs).
+struct Prof {
+  bool on = false;
+  std::map<std::string, double> ms;
+  std::chrono::steady_clock::time_point t0;
+  cudaStream_t s = nullptr;
+  void begin(cudaStream_t st) { if (!on) return; s = st; cudaStreamSynchronize(s); t0 = std::chrono::steady_clock::now(); }
+  void end(const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    ms[name] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  void dump(const char* title) {
+    if (!on) return;
+    fprintf(stderr, "[aifmm profile] %s:", title);
+    for (auto& kv : ms) fprintf(stderr, " %s=%.2fms", kv.first.c_str(), kv.second);
+    fprintf(stderr, "\n");
+    ms.clear();
+  }
+};
+inline Prof g_prof;
 
 // ---------------------------------------------------------------------------------- pools
 // Chunked bump allocator of device memory.  Blocks live until reset()/release().
@@ -66,6 +92,9 @@ class DevPool {
   double* d(size_t n) { return static_cast<double*>(alloc(n * sizeof(double))); }
   int* i(size_t n) { return static_cast<int*>(alloc(n * sizeof(int))); }
   void reset() { cur_ = 0; used_ = 0; if (chunks_.empty()) cur_ = 0; }
+  // recycle: forget every allocation but keep the chunks cached for the next build (a caching
+  // allocator: cudaMalloc/cudaFree stay out of repeated build/factor cycles)
+  void recycle() { reset(); }
   void release() {
     for (void* p : chunks_) cudaFree(p);
     chunks_.clear();
@@ -397,7 +426,9 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
   const void* dt = up.put(tb.data(), tb.size());
   double* const* douts = up.put(outs);
   const int* dldo = up.put(ldo);
+  if (g_prof.on) { g_prof.end("cmp.proj"); g_prof.begin(s); }
   for (int j = 0; j < rmax; j += HH_PANEL) {
+    if (g_prof.on) g_prof.begin(s);
     if (nsmall) launch_hh_panel(dt, (int)nsmall, j, s, 0, 0);
     if (nmid) launch_hh_panel(static_cast<const char*>(dt) + nsmall * tsz, (int)nmid, j, s, 2, nmax_mid);
     if (reqs.size() > nsmall + nmid)
@@ -419,10 +450,13 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
       g3.task(C, q.lda, q.n - j, nc, 1.0);
       g3.term(-1.0, V[i], q.n, 0, Z2[i], HH_PANEL, 0, nbw);
     }
+    if (g_prof.on) { g_prof.end("hh.panel"); g_prof.begin(s); }
     g1.run(up, s);
     g2.run(up, s);
     g3.run(up, s);
+    if (g_prof.on) g_prof.end("hh.trail");
   }
+  if (g_prof.on) g_prof.begin(s);
   launch_hh_extract(dt, (int)reqs.size(), douts, dldo, s);
 }
 // run pivoted-QR tasks: tall ones (m >= 128) on 8-CTA clusters, the rest one CTA each
