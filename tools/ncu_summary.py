@@ -9,7 +9,7 @@ for r in rows[hdr_i + 1:]:
     if len(r) <= vi: continue
     try: v = float(r[vi].replace(",", ""))
     except ValueError: continue
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}.get(r[ui], 1.0)
     name = r[ki].split("(")[0]
     tot[name] += v * scale; cnt[name] += 1
 T = sum(tot.values())
