@@ -2,7 +2,8 @@
 
 Eq. NCA (P:347-357):
     A(t^X, s^Y) ~= A(t^X, s^{X,i}) A(t^{X,i}, s^{X,i})^{-1} A(t^{X,i}, s^{Y,o}) A(t^{Y,o}, s^{Y,o})^{-1} A(t^{Y,o}, s^Y)
-with row pivots t^{X,i} in t^X and far pivots s^{X,i} in F^{X,i} = points of IL(X) (Eq. Fj).
+with row pivots t^{X,i} in t^X and far pivots s^{X,i} in F^{X,i} = sources of IL(X) (Eq. Fj, P:353;
+R11b: points of the IL boxes at the leaf level, their children's skeletons above).
 Operators: U_B = A(t^B, s^{B,i}) A(t^{B,i}, s^{B,i})^{-1} (L2P, stacked L2L at
 non-leaf levels, Table P:420-428); V_B^* = A(t^{B,o}, s^{B,o})^{-1} A(t^{B,o}, s^B) (P2M / M2M);
 M2L A_BD = A(t^{B,i}, s^{D,o}); near K_BX = A(t^B, s^X).
@@ -97,17 +98,30 @@ class NNCA:
             for B in sorted(near[l]):
                 if l == tree.L:
                     a, b = tree.point_range(l, B)
-                    R = np.arange(a, b, dtype=np.int64)
+                    self.R[l][B] = np.arange(a, b, dtype=np.int64)
                 else:
                     parts = [self.sk[l + 1][c] for c in tree.children(l, B)]
-                    R = np.concatenate(parts) if parts else np.zeros(0, np.int64)
-                F = [np.arange(*tree.point_range(l, D), dtype=np.int64) for D in il[l][B]]
-                # R20: a sparse neighbourhood can leave IL(B) with fewer points than R_B; then
-                # the IL of the ancestors (coarser far field of B) is appended, parent first
+                    self.R[l][B] = np.concatenate(parts) if parts else np.zeros(0, np.int64)
+            for B in sorted(near[l]):
+                R = self.R[l][B]
+                # R11b: the sources s^{X'} of an IL box X' at level l are its x-variables, i.e.
+                # its points at the leaf level and its children's skeletons above (Eq. Fj
+                # with Eq. P:414-416) -- the same sets as the candidate rows R_{X'}
+                F = [self.R[l][D] for D in il[l][B]]
+                # R20: a sparse neighbourhood can leave IL(B) with fewer sources than R_B; then
+                # the IL of the ancestors (coarser far field of B) is appended, parent first,
+                # each ancestor IL box D represented by the same nested sources: its points at the
+                # leaf level, else the skeletons of its level-(l+1) descendants (Morton order)
                 la, A_ = l, B
                 while sum(f.size for f in F) < R.size and la > 2:
                     la, A_ = la - 1, A_ >> tree.d
-                    F += [np.arange(*tree.point_range(la, D), dtype=np.int64) for D in il[la][A_]]
+                    for D in il[la][A_]:
+                        if l == tree.L:
+                            F.append(np.arange(*tree.point_range(la, D), dtype=np.int64))
+                        else:
+                            sh = tree.d * (l + 1 - la)
+                            F += [self.sk[l + 1][c] for c in range(D << sh, (D + 1) << sh)
+                                  if c in self.sk[l + 1]]
                 F = np.concatenate(F) if F else np.zeros(0, np.int64)
                 self.R[l][B] = R
                 if R.size == 0 or F.size == 0:

@@ -40,6 +40,7 @@ void tree_colour(const long long* offl, int nb, int ncap, const int* ncnt, const
 struct AcaTask {
   const int* R;
   const int* frange;
+  const int* fidx;
   int nR, nfr, nF, kmax;
   double* Uw;
   double* Vw;
@@ -50,6 +51,8 @@ struct AcaTask {
   int* cpiv;
 };
 void launch_aca(const AcaTask* t, int ntasks, const double* pts, KernelParams kp, double eps, cudaStream_t s);
+void launch_aca_cluster(const AcaTask* t, int ntasks, int kmax, const double* pts, KernelParams kp, double eps,
+                        cudaStream_t s);
 
 // small integer kernels
 __global__ void iota_kernel(int* dst, long long n, int base) {
@@ -103,6 +106,8 @@ struct FLevel {
   int l = 0, nb = 0;
   std::vector<int> boxes;
   std::vector<int> m, k, kP;           // kP: columns of Ud (parent NNCA rank)
+  std::vector<int> kcap;               // rank capacity of the far (M2L) blocks of a box
+  int* dinfo = nullptr;                // per-box pivot-inverse status (checked at level end)
   std::vector<double*> U, V, Ud, Vd;   // capacity: U,V m x m; Ud,Vd m x kP (ld m)
   std::vector<char> E;
   std::unordered_map<long long, Blk> nearb;   // current version of near blocks
@@ -119,7 +124,12 @@ struct Ctx {
   cudaStream_t s = nullptr;
   bool own_stream = false;
   Uploader up;
+  // persist: build outputs and the factor records the solve replays (pivot inverses, near-block
+  // versions); scratch0/1: per-level state that dies with the next level's setup (bases, M2L,
+  // far fill-ins, final near blocks), alternating by level parity; work: per-phase temporaries
   DevPool persist{(size_t)512 << 20}, work{(size_t)256 << 20}, buildp{(size_t)256 << 20};
+  DevPool scratch0{(size_t)256 << 20}, scratch1{(size_t)256 << 20};
+  DevPool& scr(int l) { return (l & 1) ? scratch1 : scratch0; }
   int d = 0, kid = 0, leaf = 0, L = 0;
   long long n = 0;
   KernelParams kp{};
@@ -304,7 +314,16 @@ static void build_nnca(Ctx& c) {
       }
       if (!ic.empty()) LAUNCH(icopy_tasks_kernel, (int)ic.size(), 128, 0, c.s, c.up.put(ic));
     }
-    // far ranges per box
+    // far sources per box (R11b): IL boxes' points at the leaf level, their children's
+    // skeletons above.  Both are ranges of one index array: the identity at the leaves, the
+    // level-(l+1) skeleton array above (whose box-ordered runs are exactly the R_D of level l).
+    const int* fidx = (l == L) ? nullptr : c.nn[l + 1].dsk;
+    auto src_range = [&](int la, int D, int* a, int* e) {
+      if (l == L) { *a = (int)c.off[la][D]; *e = (int)c.off[la][D + 1]; return; }
+      const int sh = c.d * (l + 1 - la);
+      *a = (int)c.nn[l + 1].skoff[(size_t)D << sh];
+      *e = (int)c.nn[l + 1].skoff[(size_t)(D + 1) << sh];
+    };
     std::vector<int> fr;
     std::vector<long long> froff(nb + 1, 0);
     std::vector<int> nF(nb, 0);
@@ -314,11 +333,13 @@ static void build_nnca(Ctx& c) {
       int ni;
       const int* il = c.ilist(l, b, &ni);
       for (int t = 0; t < ni; ++t) {
-        fr.push_back((int)c.off[l][il[t]]);
-        fr.push_back((int)c.off[l][il[t] + 1]);
-        nF[b] += c.count(l, il[t]);
+        int a, e;
+        src_range(l, il[t], &a, &e);
+        if (e <= a) continue;
+        if (froff[b + 1] > froff[b] && fr.back() == a) fr.back() = e;   // merge adjacent runs
+        else { fr.push_back(a); fr.push_back(e); froff[b + 1] += 1; }
+        nF[b] += e - a;
       }
-      froff[b + 1] += ni;
       // R20: sparse neighbourhoods -> append the ancestors' interaction lists
       int la = l, ab = b;
       while (nF[b] < nl.nR[b] && la > 2) {
@@ -326,11 +347,13 @@ static void build_nnca(Ctx& c) {
         ab >>= c.d;
         const int* ila = c.ilist(la, ab, &ni);
         for (int t = 0; t < ni; ++t) {
-          fr.push_back((int)c.off[la][ila[t]]);
-          fr.push_back((int)c.off[la][ila[t] + 1]);
-          nF[b] += c.count(la, ila[t]);
+          int a, e;
+          src_range(la, ila[t], &a, &e);
+          if (e <= a) continue;
+          if (froff[b + 1] > froff[b] && fr.back() == a) fr.back() = e;
+          else { fr.push_back(a); fr.push_back(e); froff[b + 1] += 1; }
+          nF[b] += e - a;
         }
-        froff[b + 1] += ni;
       }
     }
     int* dfr = fr.empty() ? nullptr : c.up.put(fr);
@@ -363,6 +386,7 @@ static void build_nnca(Ctx& c) {
           AcaTask t{};
           t.R = nl.dR + nl.Roff[b];
           t.frange = dfr + 2 * froff[b];
+          t.fidx = fidx;
           t.nR = nl.nR[b];
           t.nfr = (int)(froff[b + 1] - froff[b]);
           AIFMM_REQUIRE(t.nfr <= 256, AIFMM_EINVALID_ARG, "too many far ranges");
@@ -379,7 +403,15 @@ static void build_nnca(Ctx& c) {
         }
         ++i1;
       }
-      if (!tasks.empty()) launch_aca(c.up.put(tasks), (int)tasks.size(), c.pts, c.kp, eps, c.s);
+      // long far sets on few boxes (upper levels, 3D) go to the 8-CTA cluster kernel
+      std::vector<AcaTask> small, big;
+      int kbig = 1;
+      for (const AcaTask& t : tasks) {
+        if (t.nF >= 16384 || (boxes.size() < 512 && t.nF >= 1024)) { big.push_back(t); kbig = std::max(kbig, t.kmax); }
+        else small.push_back(t);
+      }
+      if (!small.empty()) launch_aca(c.up.put(small), (int)small.size(), c.pts, c.kp, eps, c.s);
+      if (!big.empty()) launch_aca_cluster(c.up.put(big), (int)big.size(), kbig, c.pts, c.kp, eps, c.s);
       c.up.sync();
       i0 = i1;
     }
@@ -463,7 +495,10 @@ static void setup_level(Ctx& c, int l) {
   f.Ud.assign(nb, nullptr);
   f.Vd.assign(nb, nullptr);
   f.E.assign(nb, 0);
+  f.kcap.assign(nb, 0);
   f.rec.assign(nb, Rec{});
+  DevPool& S = c.scr(l);
+  S.reset();   // held level l+2 (stream order makes the reuse safe)
   f.nearb.clear();
   f.A.clear();
   f.F.clear();
@@ -485,7 +520,11 @@ static void setup_level(Ctx& c, int l) {
     }
     f.k[b] = nl.k[b];
     f.kP[b] = (l > 2) ? c.nn[l - 1].k[b >> d] : 0;
+    // compression grows ranks by ~1-1.5x the NNCA rank (measured); regrow() handles the rest
+    f.kcap[b] = std::min(f.m[b], 2 * f.k[b] + 16);
   }
+  f.dinfo = S.i(nb);
+  AIFMM_CUDA(cudaMemsetAsync(f.dinfo, 0, sizeof(int) * nb, c.s));
   // zero-initialised capacity storage: U, V, Ud, Vd, far A, far F
   size_t zbytes = 0;
   auto rnd = [](size_t x) { return (x * 8 + 255) & ~(size_t)255; };
@@ -494,11 +533,11 @@ static void setup_level(Ctx& c, int l) {
     int ni;
     const int* il = c.ilist(l, b, &ni);
     for (int t = 0; t < ni; ++t) {
-      zbytes += rnd((size_t)f.m[b] * f.m[il[t]]);
+      zbytes += rnd((size_t)f.kcap[b] * f.kcap[il[t]]);
       if (c.cheb(l, b, il[t]) == 2) zbytes += rnd((size_t)f.m[b] * f.m[il[t]]);
     }
   }
-  char* z = static_cast<char*>(c.persist.alloc(std::max<size_t>(zbytes, 256)));
+  char* z = static_cast<char*>(S.alloc(std::max<size_t>(zbytes, 256)));
   AIFMM_CUDA(cudaMemsetAsync(z, 0, zbytes, c.s));
   size_t zo = 0;
   auto carve = [&](size_t nel) { double* p = reinterpret_cast<double*>(z + zo); zo += rnd(nel); return p; };
@@ -511,7 +550,7 @@ static void setup_level(Ctx& c, int l) {
     const int* il = c.ilist(l, b, &ni);
     for (int t = 0; t < ni; ++t) {
       int q = il[t];
-      f.A[f.key(b, q)] = Blk{carve((size_t)f.m[b] * f.m[q]), std::max(f.m[b], 1), f.k[b], f.k[q]};
+      f.A[f.key(b, q)] = Blk{carve((size_t)f.kcap[b] * f.kcap[q]), std::max(f.kcap[b], 1), f.k[b], f.k[q]};
       if (c.cheb(l, b, q) == 2) f.F[f.key(b, q)] = Blk{carve((size_t)f.m[b] * f.m[q]), std::max(f.m[b], 1), 0, 0};
     }
   }
@@ -545,7 +584,9 @@ static void setup_level(Ctx& c, int l) {
     const int* nbl = c.nlist(l, b, &nn_);
     for (int t = 0; t < nn_; ++t) {
       int q = nbl[t];
-      Blk blk{c.persist.d(std::max<size_t>((size_t)m * f.m[q], 1)), std::max(m, 1), m, f.m[q]};
+      // the diagonal block is consumed by the pivot; off-diagonal ones are solve records
+      DevPool& bp = (q == b) ? S : c.persist;
+      Blk blk{bp.d(std::max<size_t>((size_t)m * f.m[q], 1)), std::max(m, 1), m, f.m[q]};
       f.nearb[f.key(b, q)] = blk;
       if (l == c.L) {
         kt.push_back(KEvalTask{blk.p, blk.ld, m, f.m[q], nullptr, nullptr, (int)c.off[l][b], (int)c.off[l][q]});
@@ -577,6 +618,9 @@ static void setup_level(Ctx& c, int l) {
   AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
   cb.run(c.up, c.s);
   if (!kt.empty()) launch_keval(c.up.put(kt), (int)kt.size(), 4, c.pts, c.kp, c.dflag, c.s);
+  // level l+1's per-level state is dead once copied: mark its pool free (reused by level l-1,
+  // or given back by an out-of-memory trim)
+  if (prev) c.scr(l + 1).reset();
 }
 
 // R13: U_b = Q T, V_b = Q' T'; rows of Z_b <- T (.), columns of y_b <- (.) T'^T
@@ -665,20 +709,42 @@ static void orthonormalise(Ctx& c, FLevel& f) {
   c.work.reset();
 }
 
-// Alg. 3 lines P:1118-1129 for the pending pairs S (colour-batched, R12; R14, R15)
-static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& S) {
-  std::map<int, std::vector<int>> part;
-  for (auto& pr : S) {
-    part[pr.first].push_back(pr.second);
-    part[pr.second].push_back(pr.first);
+// Far (M2L) blocks are stored with a per-box rank capacity kcap; when compression grows a box's
+// rank past it, every block in that box's Z row and y column moves to larger zero-padded storage.
+static void regrow(Ctx& c, FLevel& f, const std::vector<int>& grown) {
+  if (grown.empty()) return;
+  std::vector<int> ncap = f.kcap;
+  for (int b : grown) ncap[b] = std::min(f.m[b], std::max(f.k[b], f.kcap[b] + f.kcap[b] / 2 + 8));
+  std::set<long long> keys;
+  for (int b : grown) {
+    int ni;
+    const int* il = c.ilist(f.l, b, &ni);
+    for (int t = 0; t < ni; ++t) {
+      keys.insert(f.key(b, il[t]));
+      keys.insert(f.key(il[t], b));
+    }
   }
-  std::vector<int> aff;
-  for (auto& kv : part) {
-    std::sort(kv.second.begin(), kv.second.end());
-    if (!f.E[kv.first]) aff.push_back(kv.first);
+  DevPool& S = c.scr(f.l);
+  CopyBatch zero, mv;
+  for (long long key : keys) {
+    const int p = (int)(key / f.nb), q = (int)(key % f.nb);
+    Blk& A = f.A.at(key);
+    Blk nb_{S.d(std::max<size_t>((size_t)ncap[p] * ncap[q], 1)), std::max(ncap[p], 1), A.rows, A.cols};
+    zero.fill(nb_.p, nb_.ld, ncap[p], ncap[q], 0.0);
+    mv.copy(A.p, A.ld, nb_.p, nb_.ld, f.kcap[p], f.kcap[q]);
+    A = nb_;
   }
+  zero.run(c.up, c.s);
+  mv.run(c.up, c.s);
+  f.kcap = ncap;
+}
+
+// Phase 1 of the compression for a group of affected boxes: new basis columns (written into
+// U_b / V_b after column k_b) and the common rank growth tgt (R8, R8b, R15).  The group's
+// temporaries live in c.work; the rank read-back at the end synchronises the stream.
+static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::map<int, std::vector<int>>& part,
+                           std::vector<int>& tgt) {
   const int na = (int)aff.size();
-  if (!na) return;
   if (g_prof.on) g_prof.begin(c.s);
   // candidates stored transposed (rows = fill-in columns): WT_U = [F_bq^T ...], WT_V = [F_pb ...]
   struct Side { double* WT; int n; double* M; int r; };
@@ -775,7 +841,8 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   if (!pq.empty()) run_pqr(pq, c.up, c.s);
   std::vector<int> th = d2h(c, dt, 4 * na);
   if (g_prof.on) { g_prof.end("cmp.pqrA"); g_prof.begin(c.s); }
-  std::vector<int> tgt(na), hu(na), hv(na);
+  tgt.assign(na, 0);
+  std::vector<int> hu(na), hv(na);
   pq.clear();
   smem = 0;
   for (int a = 0; a < na; ++a) {
@@ -847,18 +914,64 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   for (int a = 0; a < na; ++a)
     AIFMM_REQUIRE(haveU[a] == tgt[a] && haveV[a] == tgt[a], AIFMM_ESINGULAR_PIVOT, "rank equalisation failed");
   if (g_prof.on) { g_prof.end("cmp.pqrB"); g_prof.begin(c.s); }
+}
+
+// Alg. 3 lines P:1118-1129 for the pending pairs S (colour-batched, R12; R14, R15)
+static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& S) {
+  std::map<int, std::vector<int>> part;
+  for (auto& pr : S) {
+    part[pr.first].push_back(pr.second);
+    part[pr.second].push_back(pr.first);
+  }
+  std::vector<int> aff;
+  for (auto& kv : part) {
+    std::sort(kv.second.begin(), kv.second.end());
+    if (!f.E[kv.first]) aff.push_back(kv.first);
+  }
+  const int na = (int)aff.size();
+  if (!na) return;
+  if (g_prof.on) g_prof.begin(c.s);
+  // phase 1 in groups whose temporaries stay under a workspace budget
+  std::vector<int> tgt(na, 0);
+  {
+    const double budget = 6e9;
+    size_t a0 = 0;
+    while (a0 < aff.size()) {
+      double ws = 0.0;
+      size_t a1 = a0;
+      while (a1 < aff.size()) {
+        const int b = aff[a1], m = f.m[b];
+        int nu = 0;
+        for (int q : part[b]) nu += live(f, q);
+        const double need = 8.0 * (4.0 * nu * m + 2.0 * m * m + 2.0 * nu * 32 + 4.0 * 32 * m) + 4096.0;
+        if (a1 > a0 && ws + need > budget) break;
+        ws += need;
+        ++a1;
+      }
+      std::vector<int> grp(aff.begin() + a0, aff.begin() + a1), tg;
+      compress_boxes(c, f, grp, part, tg);
+      for (size_t t = 0; t < grp.size(); ++t) tgt[a0 + t] = tg[t];
+      c.work.reset();
+      a0 = a1;
+    }
+  }
   // new ranks
+  std::vector<int> grown;
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
     f.k[b] += tgt[a];
+    if (f.k[b] > f.kcap[b]) grown.push_back(b);
     c.stats[AIFMM_STAT_COMPRESSIONS] += 1;
   }
+  regrow(c, f, grown);
   for (auto& kv : f.A) {
     int p = (int)(kv.first / f.nb), q = (int)(kv.first % f.nb);
     kv.second.rows = f.k[p];
     kv.second.cols = f.k[q];
   }
   // redirection: A_xy += U~_x^* F_xy V~_y  (P2P) | F V~ (P2L) | U~^* F (M2P)
+  GemmBatch g;
+  CopyBatch cb;
   std::vector<std::pair<std::pair<int, int>, double*>> p2p;
   for (auto& pr : S)
     for (int dir = 0; dir < 2; ++dir) {
@@ -903,7 +1016,6 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
   // 1. assemble P_i = [[K_ii, U_i],[V_i^T, 0]] into G_i and invert in place (R16)
   CopyBatch cb;
   std::vector<InvReq> inv;
-  int* dinfo = c.work.i(cs.size());
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];
     const int m = f.m[i], k = f.k[i], n = m + k;
@@ -917,10 +1029,9 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
     cb.copy(f.U[i], m, r.G + (size_t)m * n, n, m, k);
     cb.copy(f.V[i], m, r.G + m, n, k, m, 1.0, 1);
     cb.fill(r.G + (size_t)m * n + m, n, k, k, 0.0);
-    inv.push_back(InvReq{r.G, n, n, dinfo + a});
+    inv.push_back(InvReq{r.G, n, n, f.dinfo + i});
   }
   cb.run(c.up, c.s);
-  AIFMM_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int) * cs.size(), c.s));
   batched_inverse(inv, c.work, c.up, c.s, &c.fc_all);
   if (g_prof.on) { g_prof.end("elim.inverse"); g_prof.begin(c.s); }
   // 2. W_i = G[:, 0:m] * R_i (row X_i blocks), columns ordered as N(i) \ i
@@ -992,7 +1103,9 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
       const Blk& C = f.nearb.at(f.key(p, i));
       r.C.push_back({p, C});
       r.Ckind_z.push_back(f.E[p]);
-      Blk nb_{c.persist.d(std::max<size_t>((size_t)live(f, p) * k, 1)), std::max(live(f, p), 1), live(f, p), k};
+      // (X_p, y_i) is replayed by the solve when p is eliminated; (Z_p, y_i) is final
+      DevPool& bp = f.E[p] ? c.scr(l) : c.persist;
+      Blk nb_{bp.d(std::max<size_t>((size_t)live(f, p) * k, 1)), std::max(live(f, p), 1), live(f, p), k};
       if (live(f, p) && k) {
         g.task(nb_.p, nb_.ld, live(f, p), k, 0.0);
         if (m) g.term(1.0, C.p, C.ld, 0, r.G + (size_t)m * n, n, 0, m);
@@ -1003,11 +1116,12 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
       const Blk& R = f.nearb.at(f.key(i, q));
       r.R.push_back({q, R});
       r.Rkind_y.push_back(f.E[q]);
-      Blk nb_{c.persist.d(std::max<size_t>((size_t)k * live(f, q), 1)), std::max(k, 1), k, live(f, q)};
+      DevPool& bp = f.E[q] ? c.scr(l) : c.persist;
+      Blk nb_{bp.d(std::max<size_t>((size_t)k * live(f, q), 1)), std::max(k, 1), k, live(f, q)};
       cb.copy(W[a] + (size_t)wcol[a][q] * n + m, n, nb_.p, nb_.ld, k, live(f, q));
       fresh.push_back({f.key(i, q), nb_});
     }
-    Blk nb_{c.persist.d(std::max<size_t>((size_t)k * k, 1)), std::max(k, 1), k, k};
+    Blk nb_{c.scr(l).d(std::max<size_t>((size_t)k * k, 1)), std::max(k, 1), k, k};
     cb.copy(r.G + (size_t)m * n + m, n, nb_.p, nb_.ld, k, k, -1.0);
     fresh.push_back({f.key(i, i), nb_});
   }
@@ -1029,11 +1143,7 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
   if (g_prof.on) { g_prof.end("elim.schur"); g_prof.begin(c.s); }
   for (auto& fr : fresh) f.nearb[fr.first] = fr.second;
   for (int i : cs) f.E[i] = 1;
-  std::vector<int> info = d2h(c, dinfo, cs.size());
-  for (size_t a = 0; a < cs.size(); ++a)
-    if (info[a])
-      throw Error(AIFMM_ESINGULAR_PIVOT, "singular pivot at level " + std::to_string(l) + " box " + std::to_string(cs[a]));
-  c.work.reset();
+  c.work.reset();   // stream order: the next colour's temporaries are written after these reads
   if (g_prof.on) g_prof.end("elim.tail");
 }
 
@@ -1066,12 +1176,20 @@ static void factor_all(Ctx& c) {
       g_prof.end(("eliminate.L" + std::to_string(l)).c_str());
     }
     AIFMM_REQUIRE(f.pending.empty(), AIFMM_ESINGULAR_PIVOT, "pending far fill-ins at level end");
+    {
+      std::vector<int> info = d2h(c, f.dinfo, f.nb);
+      for (int b : f.boxes)
+        if (info[b])
+          throw Error(AIFMM_ESINGULAR_PIVOT, "singular pivot at level " + std::to_string(l) + " box " + std::to_string(b));
+    }
     if (g_prof.on) {
       double ms = 0, mx = 0, ks = 0, kx = 0, k0s = 0;
       for (int b : f.boxes) { ms += f.m[b]; mx = std::max(mx, (double)f.m[b]); ks += f.k[b]; kx = std::max(kx, (double)f.k[b]); k0s += c.nn[l].k[b]; }
       double nbx = (double)f.boxes.size();
-      fprintf(stderr, "[aifmm profile] level %d boxes %d m avg %.1f max %.0f | k nnca avg %.1f final avg %.1f max %.0f\n",
-              l, (int)nbx, ms / nbx, mx, k0s / nbx, ks / nbx, kx);
+      fprintf(stderr, "[aifmm profile] level %d boxes %d m avg %.1f max %.0f | k nnca avg %.1f final avg %.1f max %.0f"
+              " | GB persist %.2f/%.2f scratch %.2f+%.2f work %.2f\n",
+              l, (int)nbx, ms / nbx, mx, k0s / nbx, ks / nbx, kx, c.persist.in_use() / 1e9, c.persist.total() / 1e9,
+              c.scratch0.total() / 1e9, c.scratch1.total() / 1e9, c.work.total() / 1e9);
     }
     for (int b : f.boxes) c.stats[AIFMM_STAT_MAX_RANK] = std::max(c.stats[AIFMM_STAT_MAX_RANK], (double)f.k[b]);
     // solve layout
@@ -1295,6 +1413,8 @@ int aifmm_build(const double* points, int64_t n, int d, int kernel_id, const dou
   auto t0 = std::chrono::steady_clock::now();
   c.persist.recycle();
   c.buildp.recycle();
+  c.scratch0.recycle();
+  c.scratch1.recycle();
   c.work.reset();
   c.fl.clear();
   c.nn.clear();
@@ -1357,7 +1477,8 @@ int aifmm_factor(void) {
   c.stats[AIFMM_STAT_FACTOR_FLOPS] = c.fc_all.flops + c.fc_schur.flops;
   c.factored = true;
   c.stats[AIFMM_STAT_FACTOR_MS] = ms_since(t0);
-  c.stats[AIFMM_STAT_DEVICE_BYTES] = (double)c.persist.total();
+  c.stats[AIFMM_STAT_DEVICE_BYTES] =
+      (double)(c.persist.total() + c.scratch0.total() + c.scratch1.total() + c.work.total() + c.buildp.total());
   CAPI_END
 }
 
@@ -1405,6 +1526,8 @@ void aifmm_free(void) {
   c.nn.clear();
   // device memory stays cached in the pools (released at process exit or by a failing build)
   c.persist.recycle();
+  c.scratch0.recycle();
+  c.scratch1.recycle();
   c.work.reset();
   c.buildp.recycle();
   c.built = c.factored = false;

@@ -242,14 +242,18 @@ __device__ int gj_device(double* M, int ld, int n, int nc, int mode, double* f, 
       else M[(size_t)j * ld + k] *= d;
     }
     __syncthreads();
-    const int ncol = jhi - jlo;
-    const int tot = ncol * n;
-    for (int e = tid; e < tot; e += GJ_NT) {
-      const int i = e % n, j = jlo + e / n;
-      if (i == k) continue;
-      const double fi = f[i];
-      if (j == k) M[(size_t)j * ld + i] = (mode == 1) ? -fi * d : 0.0;
-      else M[(size_t)j * ld + i] -= fi * M[(size_t)j * ld + k];
+    // rank-1 update, one warp per column (rows contiguous: no integer division per element)
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int j = jlo + warp; j < jhi; j += GJ_NT / 32) {
+      double* col = M + (size_t)j * ld;
+      if (j == k) {
+        for (int i = lane; i < n; i += 32)
+          if (i != k) col[i] = (mode == 1) ? -f[i] * d : 0.0;
+      } else {
+        const double mk = col[k];
+        for (int i = lane; i < n; i += 32)
+          if (i != k) col[i] -= f[i] * mk;
+      }
     }
     __syncthreads();
   }

@@ -31,7 +31,7 @@ void hh_make(void* out, double* A, int lda, int n, int m, double* V, double* T);
 void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode, int nmax);
 void launch_hh_extract(const void* t, int ntasks, double* const* out, const int* ldo, cudaStream_t s);
 constexpr int HH_PANEL = 32;
-constexpr int GJ_SMALL_MAX = 80;   // in-place inverses up to this size run in shared memory
+constexpr int GJ_SMALL_MAX = 160;  // in-place inverses up to this size run in shared memory (<= 206 KB)
 constexpr int GJ_PANEL = 32;
 
 // Optional phase profile (AIFMM_PROFILE=1): synchronises at phase boundaries and prints a
@@ -58,11 +58,25 @@ struct Prof {
 inline Prof g_prof;
 
 // ---------------------------------------------------------------------------------- pools
-// Chunked bump allocator of device memory.  Blocks live until reset()/release().
+// Chunked bump allocator of device memory.  Blocks live until reset()/release().  Chunks are
+// cached across reset() (so repeated build/factor cycles stay out of cudaMalloc/cudaFree);
+// under memory pressure every registered pool gives back its chunks that hold no live block
+// (trim) and the allocation is retried once.
+class DevPool;
+inline std::vector<DevPool*>& pool_registry() {
+  static std::vector<DevPool*> r;
+  return r;
+}
 class DevPool {
  public:
-  explicit DevPool(size_t chunk = (size_t)256 << 20) : chunk_(chunk) {}
-  ~DevPool() { release(); }
+  explicit DevPool(size_t chunk = (size_t)256 << 20) : chunk_(chunk) { pool_registry().push_back(this); }
+  ~DevPool() {
+    release();
+    auto& r = pool_registry();
+    r.erase(std::remove(r.begin(), r.end(), this), r.end());
+  }
+  DevPool(const DevPool&) = delete;
+  DevPool& operator=(const DevPool&) = delete;
   void* alloc(size_t bytes) {
     bytes = (bytes + 255) & ~(size_t)255;
     if (bytes == 0) bytes = 256;
@@ -81,21 +95,43 @@ class DevPool {
     }
     size_t sz = std::max(chunk_, bytes);
     void* p = nullptr;
-    AIFMM_CUDA(cudaMalloc(&p, sz));
-    chunks_.push_back(p);
-    sizes_.push_back(sz);
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      for (DevPool* q : pool_registry()) q->trim();
+      e = cudaMalloc(&p, sz);
+    }
+    AIFMM_CUDA(e);
+    // keep the chunk list ordered by use: a new chunk goes right after the current one
+    const size_t at = chunks_.empty() ? 0 : cur_ + 1;
+    chunks_.insert(chunks_.begin() + at, p);
+    sizes_.insert(sizes_.begin() + at, sz);
     total_ += sz;
-    cur_ = chunks_.size() - 1;
+    cur_ = at;
     used_ = bytes;
     return p;
   }
   double* d(size_t n) { return static_cast<double*>(alloc(n * sizeof(double))); }
   int* i(size_t n) { return static_cast<int*>(alloc(n * sizeof(int))); }
-  void reset() { cur_ = 0; used_ = 0; if (chunks_.empty()) cur_ = 0; }
+  void reset() { cur_ = 0; used_ = 0; }
   // recycle: forget every allocation but keep the chunks cached for the next build (a caching
   // allocator: cudaMalloc/cudaFree stay out of repeated build/factor cycles)
   void recycle() { reset(); }
+  // give back the cached chunks that hold no live block (those after the current one)
+  void trim() {
+    if (chunks_.empty()) return;
+    const size_t keep = (used_ == 0 && cur_ == 0) ? 0 : cur_ + 1;
+    if (keep < chunks_.size()) cudaDeviceSynchronize();
+    for (size_t c = keep; c < chunks_.size(); ++c) {
+      cudaFree(chunks_[c]);
+      total_ -= sizes_[c];
+    }
+    chunks_.resize(keep);
+    sizes_.resize(keep);
+    if (keep == 0) { cur_ = 0; used_ = 0; }
+  }
   void release() {
+    if (!chunks_.empty()) cudaDeviceSynchronize();
     for (void* p : chunks_) cudaFree(p);
     chunks_.clear();
     sizes_.clear();
@@ -104,6 +140,11 @@ class DevPool {
     total_ = 0;
   }
   size_t total() const { return total_; }
+  size_t in_use() const {
+    size_t u = used_;
+    for (size_t c = 0; c < cur_ && c < sizes_.size(); ++c) u += sizes_[c];
+    return u;
+  }
 
  private:
   size_t chunk_;
