@@ -103,6 +103,25 @@ int aifmm_get_colours(int level, int32_t* colour);
  * factorization (which = 1) of every box (0 for empty boxes). */
 int aifmm_get_ranks(int level, int which, int32_t* ranks);
 
+/* ---- Row a8 (BASELINE config 5): H2 matvec and AIFMM-preconditioned GMRES --------------
+ * aifmm_matvec_build — build a second NNCA (ACA tolerance tol/100, reading R18) on the tree of
+ *   the last aifmm_build, for the H2 matrix-vector product (Eq. NCA P:347-367 with the nested
+ *   operators of Table; §5 Exp. 5 uses an FMM matvec inside GMRES,
+ *   P:1628-1707).  Requires aifmm_build.  Owned by the library until the next build / free.
+ * aifmm_matvec — Y = A_H2 X.  X, Y: device, N x nrhs column-major (ld N), user point order;
+ *   X is read, Y is overwritten; they must not alias.  Near field and M2L kernel entries are
+ *   evaluated on the fly (never stored).  AIFMM_ESTATE before aifmm_matvec_build.
+ * aifmm_gmres — solve A x = b by restarted GMRES(restart) (modified Gram-Schmidt, Givens),
+ *   matrix = the H2 matvec, right preconditioner = the AIFMM factorization (aifmm_solve) when
+ *   precond != 0 (requires aifmm_factor), stopping when ||b - A x|| / ||b|| <= rtol (Arnoldi
+ *   estimate inside a cycle, true residual at each restart) or after maxit iterations.
+ *   b (read) and x (written): device, N doubles, user order.  iters / relres: host out.
+ *   AIFMM_ENONFINITE for a non-finite b. */
+int aifmm_matvec_build(double tol);
+int aifmm_matvec(const double* X, double* Y, int nrhs);
+int aifmm_gmres(const double* b, double* x, int restart, double rtol, int maxit, int precond,
+                int* iters, double* relres);
+
 /* aifmm_stats — host double[AIFMM_NSTATS], see the AIFMM_STAT_* indices. */
 #define AIFMM_NSTATS 16
 #define AIFMM_STAT_BUILD_MS        0

@@ -22,7 +22,7 @@ SYMBOLS = ["aifmm_build", "aifmm_set_compression_tol", "aifmm_factor", "aifmm_so
            "aifmm_solve_host", "aifmm_free", "aifmm_last_error", "aifmm_set_stream",
            "aifmm_get_tree", "aifmm_get_level_offsets", "aifmm_get_lists", "aifmm_get_colours",
            "aifmm_get_ranks", "aifmm_stats", "aifmm_reset_counters", "aifmm_set_timing",
-           "aifmm_debug_inverse"]
+           "aifmm_debug_inverse", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres"]
 STAT_NAMES = ["build_ms", "factor_ms", "solve_ms", "levels", "top_size", "factor_flops",
               "schur_flops", "schur_ms", "launches", "compressions", "max_rank", "device_bytes",
               "schur_bytes", "schur_launches", "solve_bytes", "host_syncs"]
@@ -62,6 +62,9 @@ def load(path: str = LIB_PATH):
     lib.aifmm_stats.argtypes = [P]
     lib.aifmm_set_timing.argtypes = [I]
     lib.aifmm_debug_inverse.argtypes = [P, I, I]
+    lib.aifmm_matvec_build.argtypes = [D]
+    lib.aifmm_matvec.argtypes = [P, P, I]
+    lib.aifmm_gmres.argtypes = [P, P, I, D, I, I, P, P]
     _lib = lib
     return lib
 
@@ -187,3 +190,33 @@ def debug_inverse(M):
     Mc = M.to(torch.float64).t().contiguous()   # column-major storage of M
     _check(load().aifmm_debug_inverse(ctypes.c_void_p(Mc.data_ptr()), Mc.shape[0], Mc.shape[0]))
     return Mc.t()
+
+
+def matvec_build(tol: float):
+    """Second NNCA at the matvec tolerance (row a8); requires build()."""
+    _check(load().aifmm_matvec_build(float(tol)))
+
+
+def matvec(X):
+    """Y = A_H2 X for a torch.cuda float64 tensor X (N,) or (N, nrhs); returns a new tensor."""
+    import torch
+    one = X.dim() == 1
+    Xm = X[:, None] if one else X
+    Xf = Xm.to(torch.float64).t().contiguous()      # (nrhs, N) row-major == N x nrhs column-major
+    Yf = torch.empty_like(Xf)
+    _check(load().aifmm_matvec(ctypes.c_void_p(Xf.data_ptr()), ctypes.c_void_p(Yf.data_ptr()), int(Xf.shape[0])))
+    Y = Yf.t()
+    return Y[:, 0].contiguous() if one else Y.contiguous()
+
+
+def gmres(b, restart: int = 30, rtol: float = 1e-10, maxit: int = 1000, precond: bool = True):
+    """GMRES(restart) with the H2 matvec and (optionally) the AIFMM factor as right
+    preconditioner; b: torch.cuda float64 (N,).  Returns (x, iterations, relative residual)."""
+    import torch
+    bc = b.contiguous()
+    x = torch.empty_like(bc)
+    it = ctypes.c_int(0)
+    rr = ctypes.c_double(0.0)
+    _check(load().aifmm_gmres(ctypes.c_void_p(bc.data_ptr()), ctypes.c_void_p(x.data_ptr()), int(restart), float(rtol),
+                              int(maxit), 1 if precond else 0, ctypes.byref(it), ctypes.byref(rr)))
+    return x, it.value, rr.value

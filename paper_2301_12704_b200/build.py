@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libaifmm.so")
-SOURCES = ["dense_kernels.cu", "tree_kernels.cu", "nnca_kernels.cu", "aifmm.cu"]
+SOURCES = ["dense_kernels.cu", "tree_kernels.cu", "nnca_kernels.cu", "h2_kernels.cu", "aifmm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]

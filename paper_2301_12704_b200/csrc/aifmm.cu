@@ -53,6 +53,17 @@ struct AcaTask {
 void launch_aca(const AcaTask* t, int ntasks, const double* pts, KernelParams kp, double eps, cudaStream_t s);
 void launch_aca_cluster(const AcaTask* t, int ntasks, int kmax, const double* pts, KernelParams kp, double eps,
                         cudaStream_t s);
+struct KmvTarget { const int* rows; int row0, nr; double* y; int ldy; int src_begin, src_end; };
+struct KmvSource { const int* cols; int col0, nc; const double* x; int ldx; int pad; };
+void launch_kmv(const KmvTarget* t, const KmvSource* s, int ntargets, const double* pts, KernelParams kp, int nrhs,
+                int accumulate, cudaStream_t st);
+void vec_dot(const double* a, const double* b, long long n, double* part, double* out, int sqrt_mode, cudaStream_t s);
+void vec_axpy(double* y, const double* x, long long n, const double* alpha, double sign, double beta, cudaStream_t s);
+void vec_scale_div(double* y, const double* x, long long n, const double* den, cudaStream_t s);
+void gm_givens(double* H, int ldh, double* cs, double* sn, double* g, int j, double* res, cudaStream_t s);
+void gm_backsub(const double* H, int ldh, const double* g, double* y, int k, cudaStream_t s);
+void gm_gemv(const double* V, long long ldv, const double* y, int k, long long n, double* out, cudaStream_t s);
+void set_scalar(double* dst, const double* src, double value, cudaStream_t s);
 
 // small integer kernels
 __global__ void iota_kernel(int* dst, long long n, int base) {
@@ -130,6 +141,11 @@ struct Ctx {
   DevPool persist{(size_t)512 << 20}, work{(size_t)256 << 20}, buildp{(size_t)256 << 20};
   DevPool scratch0{(size_t)256 << 20}, scratch1{(size_t)256 << 20};
   DevPool& scr(int l) { return (l & 1) ? scratch1 : scratch0; }
+  // H2 matvec (row a8): a second NNCA at the matvec tolerance on the same tree
+  std::vector<NLevel> hnn;
+  bool h2_built = false;
+  double h2_tol = 0;
+  DevPool h2pool, h2work, gmpool;
   int d = 0, kid = 0, leaf = 0, L = 0;
   long long n = 0;
   KernelParams kp{};
@@ -278,12 +294,12 @@ static void build_tree(Ctx& c, const double* user_pts) {
   }
 }
 
-static void build_nnca(Ctx& c) {
+// NNCA operators of every level into `nnv` (device arrays from `pool`), ACA tolerance eps.
+static void build_nnca(Ctx& c, std::vector<NLevel>& nnv, double eps, DevPool& pool) {
   const int L = c.L;
-  c.nn.assign(L + 1, NLevel{});
-  const double eps = c.tol / 100.0;   // reading R18
+  nnv.assign(L + 1, NLevel{});
   for (int l = L; l >= 2; --l) {
-    NLevel& nl = c.nn[l];
+    NLevel& nl = nnv[l];
     const int nb = 1 << (c.d * l);
     nl.k.assign(nb, 0);
     nl.nR.assign(nb, 0);
@@ -297,12 +313,12 @@ static void build_nnca(Ctx& c) {
       if (c.nonempty(l, b)) {
         if (l == L) r = c.count(l, b);
         else
-          for (int ch = 0; ch < (1 << c.d); ++ch) r += c.nn[l + 1].k[(b << c.d) | ch];
+          for (int ch = 0; ch < (1 << c.d); ++ch) r += nnv[l + 1].k[(b << c.d) | ch];
       }
       nl.nR[b] = r;
       nl.Roff[b + 1] = nl.Roff[b] + r;
     }
-    nl.dR = c.persist.i(std::max<long long>(nl.Roff[nb], 1));
+    nl.dR = pool.i(std::max<long long>(nl.Roff[nb], 1));
     {
       // leaf rows are point ranges; above, the children's skeletons (children have consecutive
       // ids, so their sk arrays are one contiguous run per parent)
@@ -310,19 +326,19 @@ static void build_nnca(Ctx& c) {
       for (int b : boxes) {
         if (!nl.nR[b]) continue;
         if (l == L) ic.push_back(ICopyTask{nullptr, nl.dR + nl.Roff[b], nl.nR[b], (int)c.off[l][b]});
-        else ic.push_back(ICopyTask{c.nn[l + 1].dsk + c.nn[l + 1].skoff[(size_t)b << c.d], nl.dR + nl.Roff[b], nl.nR[b], 0});
+        else ic.push_back(ICopyTask{nnv[l + 1].dsk + nnv[l + 1].skoff[(size_t)b << c.d], nl.dR + nl.Roff[b], nl.nR[b], 0});
       }
       if (!ic.empty()) LAUNCH(icopy_tasks_kernel, (int)ic.size(), 128, 0, c.s, c.up.put(ic));
     }
     // far sources per box (R11b): IL boxes' points at the leaf level, their children's
     // skeletons above.  Both are ranges of one index array: the identity at the leaves, the
     // level-(l+1) skeleton array above (whose box-ordered runs are exactly the R_D of level l).
-    const int* fidx = (l == L) ? nullptr : c.nn[l + 1].dsk;
+    const int* fidx = (l == L) ? nullptr : nnv[l + 1].dsk;
     auto src_range = [&](int la, int D, int* a, int* e) {
       if (l == L) { *a = (int)c.off[la][D]; *e = (int)c.off[la][D + 1]; return; }
       const int sh = c.d * (l + 1 - la);
-      *a = (int)c.nn[l + 1].skoff[(size_t)D << sh];
-      *e = (int)c.nn[l + 1].skoff[(size_t)(D + 1) << sh];
+      *a = (int)nnv[l + 1].skoff[(size_t)D << sh];
+      *e = (int)nnv[l + 1].skoff[(size_t)(D + 1) << sh];
     };
     std::vector<int> fr;
     std::vector<long long> froff(nb + 1, 0);
@@ -358,7 +374,7 @@ static void build_nnca(Ctx& c) {
     }
     int* dfr = fr.empty() ? nullptr : c.up.put(fr);
     // ACA in chunks bounded by workspace
-    int* drank = c.persist.i(nb);
+    int* drank = pool.i(nb);
     AIFMM_CUDA(cudaMemsetAsync(drank, 0, sizeof(int) * nb, c.s));
     std::vector<long long> kmaxv(nb, 0);
     long long pivtot = 0;
@@ -368,8 +384,8 @@ static void build_nnca(Ctx& c) {
       pivoff[b + 1] = pivoff[b] + kmaxv[b];
     }
     pivtot = pivoff[nb];
-    int* drp = c.persist.i(std::max<long long>(pivtot, 1));
-    int* dcp = c.persist.i(std::max<long long>(pivtot, 1));
+    int* drp = pool.i(std::max<long long>(pivtot, 1));
+    int* dcp = pool.i(std::max<long long>(pivtot, 1));
     const size_t budget = (size_t)6 << 30;
     size_t i0 = 0;
     while (i0 < boxes.size()) {
@@ -420,8 +436,8 @@ static void build_nnca(Ctx& c) {
     // skeleton / far-pivot arrays compacted by box
     nl.skoff.assign(nb + 1, 0);
     for (int b = 0; b < nb; ++b) nl.skoff[b + 1] = nl.skoff[b] + nl.k[b];
-    nl.dsk = c.persist.i(std::max<long long>(nl.skoff[nb], 1));
-    nl.dfp = c.persist.i(std::max<long long>(nl.skoff[nb], 1));
+    nl.dsk = pool.i(std::max<long long>(nl.skoff[nb], 1));
+    nl.dfp = pool.i(std::max<long long>(nl.skoff[nb], 1));
     {
       std::vector<ICopyTask> ic;
       for (int b : boxes) {
@@ -435,7 +451,7 @@ static void build_nnca(Ctx& c) {
     // inverse: A(fp,sk) can be ill-conditioned), U = X^T (R10: V = U)
     nl.Uoff.assign(nb + 1, 0);
     for (int b = 0; b < nb; ++b) nl.Uoff[b + 1] = nl.Uoff[b] + (long long)nl.nR[b] * nl.k[b];
-    nl.dU = c.persist.d(std::max<long long>(nl.Uoff[nb], 1));
+    nl.dU = pool.d(std::max<long long>(nl.Uoff[nb], 1));
     std::vector<KEvalTask> kt;
     std::vector<GJTask> gs, gg;
     long long smem_s = 0;
@@ -476,10 +492,13 @@ static void build_nnca(Ctx& c) {
   }
 }
 
+static void build_nnca(Ctx& c) { build_nnca(c, c.nn, c.tol / 100.0, c.persist); }   // reading R18
+
 // ------------------------------------------------------------------------------------ factor
 static inline int live(const FLevel& f, int b) { return f.E[b] ? f.k[b] : f.m[b]; }
 
 static void setup_level(Ctx& c, int l) {
+  g_prof.hstart();
   FLevel& f = c.fl[l];
   const int d = c.d, nb = 1 << (d * l);
   f.l = l;
@@ -526,21 +545,16 @@ static void setup_level(Ctx& c, int l) {
   f.dinfo = S.i(nb);
   AIFMM_CUDA(cudaMemsetAsync(f.dinfo, 0, sizeof(int) * nb, c.s));
   // zero-initialised capacity storage: U, V, Ud, Vd, far A, far F
-  size_t zbytes = 0;
-  auto rnd = [](size_t x) { return (x * 8 + 255) & ~(size_t)255; };
-  for (int b : f.boxes) {
-    zbytes += 2 * rnd((size_t)f.m[b] * f.m[b]) + 2 * rnd((size_t)f.m[b] * f.kP[b]);
-    int ni;
-    const int* il = c.ilist(l, b, &ni);
-    for (int t = 0; t < ni; ++t) {
-      zbytes += rnd((size_t)f.kcap[b] * f.kcap[il[t]]);
-      if (c.cheb(l, b, il[t]) == 2) zbytes += rnd((size_t)f.m[b] * f.m[il[t]]);
-    }
-  }
-  char* z = static_cast<char*>(S.alloc(std::max<size_t>(zbytes, 256)));
-  AIFMM_CUDA(cudaMemsetAsync(z, 0, zbytes, c.s));
-  size_t zo = 0;
-  auto carve = [&](size_t nel) { double* p = reinterpret_cast<double*>(z + zo); zo += rnd(nel); return p; };
+  // zero-initialised blocks are carved from the level pool; consecutive carvings are
+  // contiguous within a chunk, so the memset runs over few ranges
+  auto rnd = [](size_t x) { return (std::max<size_t>(x * 8, 1) + 255) & ~(size_t)255; };
+  std::vector<std::pair<char*, size_t>> zr;
+  auto carve = [&](size_t nel) {
+    char* p = static_cast<char*>(S.alloc(rnd(nel)));
+    if (!zr.empty() && zr.back().first + zr.back().second == p) zr.back().second += rnd(nel);
+    else zr.push_back({p, rnd(nel)});
+    return reinterpret_cast<double*>(p);
+  };
   for (int b : f.boxes) {
     f.U[b] = carve((size_t)f.m[b] * f.m[b]);
     f.V[b] = carve((size_t)f.m[b] * f.m[b]);
@@ -554,6 +568,8 @@ static void setup_level(Ctx& c, int l) {
       if (c.cheb(l, b, q) == 2) f.F[f.key(b, q)] = Blk{carve((size_t)f.m[b] * f.m[q]), std::max(f.m[b], 1), 0, 0};
     }
   }
+  for (auto& r : zr) AIFMM_CUDA(cudaMemsetAsync(r.first, 0, r.second, c.s));
+  g_prof.hlap("setup.carve");
   // fills
   CopyBatch cb;
   std::vector<KEvalTask> kt;
@@ -615,21 +631,85 @@ static void setup_level(Ctx& c, int l) {
         kt.push_back(KEvalTask{a.p, a.ld, f.k[b], f.k[q], nl.dsk + nl.skoff[b], nl.dsk + nl.skoff[q], 0, 0});
     }
   }
+  g_prof.hlap("setup.plan");
   AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
   cb.run(c.up, c.s);
   if (!kt.empty()) launch_keval(c.up.put(kt), (int)kt.size(), 4, c.pts, c.kp, c.dflag, c.s);
+  g_prof.hlap("setup.launch");
   // level l+1's per-level state is dead once copied: mark its pool free (reused by level l-1,
   // or given back by an out-of-memory trim)
   if (prev) c.scr(l + 1).reset();
 }
 
 // R13: U_b = Q T, V_b = Q' T'; rows of Z_b <- T (.), columns of y_b <- (.) T'^T
-static void orthonormalise(Ctx& c, FLevel& f) {
-  const int l = f.l;
-  std::vector<double*> Uold(f.nb, nullptr), Vold(f.nb, nullptr), T(f.nb, nullptr), T2(f.nb, nullptr);
+// CholeskyQR2 (two passes of G = B^T B, G = R^T R, B <- B R^{-1}) for every box's U and V at
+// once: DMMA GEMMs plus one batched Cholesky; T = R2 R1 so that B_old = Q T.  Returns false if
+// a Gram matrix is not numerically positive definite (then the pivoted-QR path runs instead).
+static bool bases_cholqr2(Ctx& c, FLevel& f, std::vector<double*>& T, std::vector<double*>& T2) {
+  std::vector<int> bx;
+  int kmax = 0;
+  for (int b : f.boxes)
+    if (f.k[b]) { bx.push_back(b); kmax = std::max(kmax, f.k[b]); }
+  if (bx.empty()) return true;
+  const int nt = 2 * (int)bx.size();
+  int* dinfo = c.work.i(2 * nt);
+  AIFMM_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int) * 2 * nt, c.s));
+  std::vector<double*> B(nt), Q1(nt), G(nt), R1(nt), R1i(nt), R2(nt), R2i(nt);
+  for (int t = 0; t < nt; ++t) {
+    const int b = bx[t / 2], m = f.m[b], k = f.k[b];
+    B[t] = (t & 1) ? f.V[b] : f.U[b];
+    Q1[t] = c.work.d((size_t)m * k);
+    G[t] = c.work.d((size_t)k * k);
+    R1[t] = c.work.d((size_t)k * k);
+    R1i[t] = c.work.d((size_t)k * k);
+    R2[t] = c.work.d((size_t)k * k);
+    R2i[t] = c.work.d((size_t)k * k);
+  }
+  auto pass = [&](std::vector<double*>& src, std::vector<double*>& R, std::vector<double*>& Ri, int info0) {
+    GemmBatch g;
+    for (int t = 0; t < nt; ++t) {
+      const int b = bx[t / 2], m = f.m[b], k = f.k[b];
+      g.task(G[t], k, k, k, 0.0);
+      g.term(1.0, src[t], m, 1, src[t], m, 0, m);
+    }
+    g.run(c.up, c.s, &c.fc_all);
+    std::vector<CholTask> ct(nt);
+    for (int t = 0; t < nt; ++t) ct[t] = CholTask{G[t], R[t], Ri[t], f.k[bx[t / 2]], 0, dinfo + info0 + t};
+    launch_chol_inv(c.up.put(ct), nt, kmax, c.s);
+  };
+  pass(B, R1, R1i, 0);
+  {
+    GemmBatch g;
+    for (int t = 0; t < nt; ++t) {
+      const int b = bx[t / 2], m = f.m[b], k = f.k[b];
+      g.task(Q1[t], m, m, k, 0.0);
+      g.term(1.0, B[t], m, 0, R1i[t], k, 0, k);
+    }
+    g.run(c.up, c.s, &c.fc_all);
+  }
+  pass(Q1, R2, R2i, nt);
+  std::vector<int> info = d2h(c, dinfo, 2 * nt);
+  for (int v : info)
+    if (v) return false;
+  GemmBatch g;
+  for (int t = 0; t < nt; ++t) {
+    const int b = bx[t / 2], m = f.m[b], k = f.k[b];
+    double* Tt = c.work.d((size_t)k * k);
+    ((t & 1) ? T2 : T)[b] = Tt;
+    g.task(B[t], m, m, k, 0.0);                 // Q = Q1 R2^{-1}
+    g.term(1.0, Q1[t], m, 0, R2i[t], k, 0, k);
+    g.task(Tt, k, k, k, 0.0);                   // T = R2 R1
+    g.term(1.0, R2[t], k, 0, R1[t], k, 0, k);
+  }
+  g.run(c.up, c.s, &c.fc_all);
+  return true;
+}
+
+// pivoted Gram-Schmidt variant (fallback): Q by the RRQR kernel with tmin = tmax = k, T = Q^T B
+static void bases_pqr(Ctx& c, FLevel& f, std::vector<double*>& T, std::vector<double*>& T2) {
+  std::vector<double*> Uold(f.nb, nullptr), Vold(f.nb, nullptr);
   CopyBatch cb;
   std::vector<PqrTask> pq;
-  size_t smem = 0;
   for (int b : f.boxes) {
     const int m = f.m[b], k = f.k[b];
     if (!k) continue;
@@ -643,7 +723,6 @@ static void orthonormalise(Ctx& c, FLevel& f) {
     cb.copy(f.V[b], m, wv, m, m, k);
     pq.push_back(PqrTask{wu, f.U[b], m, m, m, k, 0, k, k, 0, nullptr, 0.0, nullptr, nullptr});
     pq.push_back(PqrTask{wv, f.V[b], m, m, m, k, 0, k, k, 0, nullptr, 0.0, nullptr, nullptr});
-    smem = std::max(smem, (size_t)k + m + k);
   }
   cb.run(c.up, c.s);
   if (!pq.empty()) run_pqr(pq, c.up, c.s);
@@ -659,6 +738,23 @@ static void orthonormalise(Ctx& c, FLevel& f) {
     g.term(1.0, f.V[b], m, 1, Vold[b], m, 0, m);
   }
   g.run(c.up, c.s, &c.fc_all);
+}
+
+static void orthonormalise(Ctx& c, FLevel& f) {
+  const int l = f.l;
+  std::vector<double*> T(f.nb, nullptr), T2(f.nb, nullptr);
+  g_prof.begin(c.s);
+  static const bool orth_pqr = getenv("AIFMM_ORTH_PQR") != nullptr;   // debug toggle
+  if (orth_pqr || !bases_cholqr2(c, f, T, T2)) {
+    c.work.reset();
+    bases_pqr(c, f, T, T2);
+    c.stats[AIFMM_STAT_HOST_SYNCS] += 0;   // (fallback taken: pivoted Gram-Schmidt bases)
+    g_prof.end("orth.pqr_fallback");
+  } else {
+    g_prof.end("orth.cholqr2");
+  }
+  CopyBatch cb;
+  GemmBatch g;
   // Ud <- T Ud, Vd <- T' Vd ; A_pq <- T_p A_pq T'_q^T
   std::vector<double*> udc(f.nb, nullptr), vdc(f.nb, nullptr);
   std::unordered_map<long long, double*> tmpA;
@@ -1060,12 +1156,14 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
   if (g_prof.on) { g_prof.end("elim.W"); g_prof.begin(c.s); }
   // 3. Schur updates, target-centric (deterministic ascending-i accumulation), + new blocks
   // (p, q, a) triples sorted by target then by a (ascending eliminated box = fixed order)
+  g_prof.hstart();
   struct Tg { long long key; int a; };
   std::vector<Tg> tgs;
   for (size_t a = 0; a < cs.size(); ++a)
     for (int p : nbs[a])
       for (int q : nbs[a]) tgs.push_back(Tg{f.key(p, q), (int)a});
   std::sort(tgs.begin(), tgs.end(), [](const Tg& x, const Tg& y) { return x.key < y.key || (x.key == y.key && x.a < y.a); });
+  g_prof.hlap("tg.sort");
   std::vector<int> grp_a;
   for (size_t t0 = 0; t0 < tgs.size();) {
     size_t t1 = t0;
@@ -1093,6 +1191,7 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
       g.term(-1.0, C.p, C.ld, 0, W[a] + (size_t)wcol[a][q] * n, n, 0, m);
     }
   }
+  g_prof.hlap("tg.tasks");
   // new blocks (p,i) = C G12, (i,q) = G21 R = W_z, (i,i) = -G22 (R17)
   std::vector<std::pair<long long, Blk>> fresh;
   for (size_t a = 0; a < cs.size(); ++a) {
@@ -1125,6 +1224,7 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
     cb.copy(r.G + (size_t)m * n + m, n, nb_.p, nb_.ld, k, k, -1.0);
     fresh.push_back({f.key(i, i), nb_});
   }
+  g_prof.hlap("fresh");
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c.timing) {
     AIFMM_CUDA(cudaEventCreate(&e0));
@@ -1187,8 +1287,8 @@ static void factor_all(Ctx& c) {
       for (int b : f.boxes) { ms += f.m[b]; mx = std::max(mx, (double)f.m[b]); ks += f.k[b]; kx = std::max(kx, (double)f.k[b]); k0s += c.nn[l].k[b]; }
       double nbx = (double)f.boxes.size();
       fprintf(stderr, "[aifmm profile] level %d boxes %d m avg %.1f max %.0f | k nnca avg %.1f final avg %.1f max %.0f"
-              " | GB persist %.2f/%.2f scratch %.2f+%.2f work %.2f\n",
-              l, (int)nbx, ms / nbx, mx, k0s / nbx, ks / nbx, kx, c.persist.in_use() / 1e9, c.persist.total() / 1e9,
+              " | GB persist %.2f (all %.2f) scratch %.2f+%.2f work %.2f\n",
+              l, (int)nbx, ms / nbx, mx, k0s / nbx, ks / nbx, kx, c.persist.total() / 1e9, chunk_cache().total() / 1e9,
               c.scratch0.total() / 1e9, c.scratch1.total() / 1e9, c.work.total() / 1e9);
     }
     for (int b : f.boxes) c.stats[AIFMM_STAT_MAX_RANK] = std::max(c.stats[AIFMM_STAT_MAX_RANK], (double)f.k[b]);
@@ -1375,6 +1475,188 @@ static void solve_dev(Ctx& c, double* B, int nrhs) {
   W.reset();
 }
 
+// ------------------------------------------------------------------------------------ H2 matvec
+// Y = A_H2 X (user order, N x nrhs column-major, device), row a8 (oracle/h2.py): upward
+// P2M/M2M as DMMA GEMMs with the NNCA operators (V = U, R10), M2L and near field as fused
+// kernel-evaluation sums (kmv_kernel), downward L2L and L2P as GEMMs.  Multipoles and locals
+// of a level are stored box-ordered (skoff), so a box's children are one contiguous run.
+static void matvec_dev(Ctx& c, const double* X, double* Y, int nrhs) {
+  const int L = c.L, d = c.d;
+  const long long n = c.n;
+  DevPool& W = c.h2work;
+  W.reset();
+  double* Xs = W.d((size_t)n * nrhs);
+  double* Ys = W.d((size_t)n * nrhs);
+  LAUNCH(permute_rows_kernel, gsz(n * nrhs), 256, 0, c.s, X, Xs, c.perm, n, nrhs, 0);
+  std::vector<double*> q(L + 1, nullptr), lc(L + 1, nullptr);
+  std::vector<int> kt(L + 1, 0);
+  for (int l = 2; l <= L; ++l) {
+    const NLevel& nl = c.hnn[l];
+    kt[l] = (int)nl.skoff[(size_t)1 << (d * l)];
+    q[l] = W.d(std::max<size_t>((size_t)kt[l] * nrhs, 1));
+    lc[l] = W.d(std::max<size_t>((size_t)kt[l] * nrhs, 1));
+  }
+  auto boxes = [&](int l) {
+    std::vector<int> v;
+    for (int b = 0; b < (1 << (d * l)); ++b)
+      if (c.nonempty(l, b)) v.push_back(b);
+    return v;
+  };
+  // upward
+  for (int l = L; l >= 2; --l) {
+    const NLevel& nl = c.hnn[l];
+    GemmBatch g;
+    for (int b : boxes(l)) {
+      const int k = nl.k[b], nR = nl.nR[b];
+      if (!k) continue;
+      g.task(q[l] + nl.skoff[b], std::max(kt[l], 1), k, nrhs, 0.0);
+      if (!nR) continue;
+      const double* src = (l == L) ? Xs + c.off[L][b] : q[l + 1] + c.hnn[l + 1].skoff[(size_t)b << d];
+      const int lds = (l == L) ? (int)n : std::max(kt[l + 1], 1);
+      g.term(1.0, nl.dU + nl.Uoff[b], nR, 1, src, lds, 0, nR);
+    }
+    g.run(c.up, c.s);
+  }
+  // M2L (all levels in one launch): l_B = sum_{D in IL(B)} A(sk_B, sk_D) q_D
+  {
+    std::vector<KmvTarget> tg;
+    std::vector<KmvSource> sr;
+    for (int l = 2; l <= L; ++l) {
+      const NLevel& nl = c.hnn[l];
+      for (int b : boxes(l)) {
+        if (!nl.k[b]) continue;
+        KmvTarget t{nl.dsk + nl.skoff[b], 0, nl.k[b], lc[l] + nl.skoff[b], std::max(kt[l], 1), (int)sr.size(), 0};
+        int ni;
+        const int* il = c.ilist(l, b, &ni);
+        for (int s = 0; s < ni; ++s) {
+          const int D = il[s];
+          if (!nl.k[D]) continue;
+          sr.push_back(KmvSource{nl.dsk + nl.skoff[D], 0, nl.k[D], q[l] + nl.skoff[D], std::max(kt[l], 1), 0});
+        }
+        t.src_end = (int)sr.size();
+        tg.push_back(t);
+      }
+    }
+    if (!tg.empty()) {
+      const KmvSource* ds = sr.empty() ? nullptr : c.up.put(sr);
+      launch_kmv(c.up.put(tg), ds, (int)tg.size(), c.pts, c.kp, nrhs, 0, c.s);
+    }
+  }
+  // downward: l_c += U_P[rows of c] l_P
+  for (int l = 2; l < L; ++l) {
+    const NLevel& nl = c.hnn[l];
+    GemmBatch g;
+    for (int b : boxes(l)) {
+      const int k = nl.k[b], nR = nl.nR[b];
+      if (!k || !nR) continue;
+      g.task(lc[l + 1] + c.hnn[l + 1].skoff[(size_t)b << d], std::max(kt[l + 1], 1), nR, nrhs, 1.0);
+      g.term(1.0, nl.dU + nl.Uoff[b], nR, 0, lc[l] + nl.skoff[b], std::max(kt[l], 1), 0, k);
+    }
+    g.run(c.up, c.s);
+  }
+  // leaf: L2P, then the near field
+  AIFMM_CUDA(cudaMemsetAsync(Ys, 0, sizeof(double) * n * nrhs, c.s));
+  {
+    const NLevel& nl = c.hnn[L];
+    GemmBatch g;
+    std::vector<KmvTarget> tg;
+    std::vector<KmvSource> sr;
+    for (int b : boxes(L)) {
+      const int k = nl.k[b], m = c.count(L, b);
+      if (k) {
+        g.task(Ys + c.off[L][b], (int)n, m, nrhs, 1.0);
+        g.term(1.0, nl.dU + nl.Uoff[b], m, 0, lc[L] + nl.skoff[b], std::max(kt[L], 1), 0, k);
+      }
+      KmvTarget t{nullptr, (int)c.off[L][b], m, Ys + c.off[L][b], (int)n, (int)sr.size(), 0};
+      int nn_;
+      const int* nbl = c.nlist(L, b, &nn_);
+      for (int s = 0; s < nn_; ++s)
+        sr.push_back(KmvSource{nullptr, (int)c.off[L][nbl[s]], c.count(L, nbl[s]), Xs + c.off[L][nbl[s]], (int)n, 0});
+      t.src_end = (int)sr.size();
+      tg.push_back(t);
+    }
+    g.run(c.up, c.s);
+    if (!tg.empty()) launch_kmv(c.up.put(tg), c.up.put(sr), (int)tg.size(), c.pts, c.kp, nrhs, 1, c.s);
+  }
+  LAUNCH(permute_rows_kernel, gsz(n * nrhs), 256, 0, c.s, Ys, Y, c.perm, n, nrhs, 1);
+  c.up.sync();
+}
+
+// Right-preconditioned GMRES(restart) with MGS Arnoldi (oracle/h2.py: gmres); A = the H2
+// matvec, M^{-1} = the AIFMM solve (if precond).  b, x: device, user order, N x 1.
+static void gmres_dev(Ctx& c, const double* b, double* x, int restart, double rtol, int maxit, int precond,
+                      int* iters, double* relres) {
+  const long long n = c.n;
+  DevPool& P = c.gmpool;
+  P.reset();
+  const int ldh = restart + 1;
+  double* V = P.d((size_t)n * (restart + 1));
+  double* w = P.d(n);
+  double* t = P.d(n);
+  double* r = P.d(n);
+  double* H = P.d((size_t)ldh * restart);
+  double* cs = P.d(restart);
+  double* sn = P.d(restart);
+  double* g = P.d(restart + 1);
+  double* y = P.d(restart);
+  double* part = P.d(512);
+  double* sc = P.d(8);   // 0: ||b||, 1: beta, 2: residual estimate
+  auto rd = [&](double* dp) {
+    double h = 0;
+    AIFMM_CUDA(cudaMemcpyAsync(&h, dp, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    AIFMM_CUDA(cudaStreamSynchronize(c.s));
+    return h;
+  };
+  AIFMM_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c.s));
+  vec_dot(b, b, n, part, sc + 0, 1, c.s);
+  const double bnorm = rd(sc + 0);
+  int it = 0;
+  if (bnorm == 0.0) { *iters = 0; *relres = 0.0; return; }
+  vec_axpy(r, b, n, nullptr, 1.0, 0.0, c.s);   // r = b - A 0
+  vec_dot(r, r, n, part, sc + 1, 1, c.s);
+  double beta = rd(sc + 1);
+  while (it < maxit && beta > rtol * bnorm) {
+    AIFMM_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * ldh * restart, c.s));
+    AIFMM_CUDA(cudaMemsetAsync(g, 0, sizeof(double) * (restart + 1), c.s));
+    set_scalar(g, sc + 1, 0.0, c.s);
+    vec_scale_div(V, r, n, sc + 1, c.s);
+    int j = 0;
+    while (j < restart && it < maxit) {
+      double* vj = V + (size_t)j * n;
+      const double* op = vj;
+      if (precond) {
+        vec_axpy(t, vj, n, nullptr, 1.0, 0.0, c.s);
+        solve_dev(c, t, 1);
+        op = t;
+      }
+      matvec_dev(c, op, w, 1);
+      for (int i = 0; i <= j; ++i) {                   // modified Gram-Schmidt
+        double* hij = H + (size_t)j * ldh + i;
+        vec_dot(w, V + (size_t)i * n, n, part, hij, 0, c.s);
+        vec_axpy(w, V + (size_t)i * n, n, hij, -1.0, 1.0, c.s);
+      }
+      double* hj1 = H + (size_t)j * ldh + j + 1;
+      vec_dot(w, w, n, part, hj1, 1, c.s);
+      vec_scale_div(V + (size_t)(j + 1) * n, w, n, hj1, c.s);
+      gm_givens(H, ldh, cs, sn, g, j, sc + 2, c.s);
+      ++j;
+      ++it;
+      if (rd(sc + 2) <= rtol * bnorm) break;
+    }
+    gm_backsub(H, ldh, g, y, j, c.s);
+    gm_gemv(V, n, y, j, n, t, c.s);
+    if (precond) solve_dev(c, t, 1);
+    vec_axpy(x, t, n, nullptr, 1.0, 1.0, c.s);
+    matvec_dev(c, x, w, 1);                            // true residual at the restart
+    vec_axpy(r, b, n, nullptr, 1.0, 0.0, c.s);
+    vec_axpy(r, w, n, nullptr, -1.0, 1.0, c.s);
+    vec_dot(r, r, n, part, sc + 1, 1, c.s);
+    beta = rd(sc + 1);
+  }
+  *iters = it;
+  *relres = beta / bnorm;
+}
+
 }  // namespace aifmm
 
 // ====================================================================================== C-ABI
@@ -1418,6 +1700,9 @@ int aifmm_build(const double* points, int64_t n, int d, int kernel_id, const dou
   c.work.reset();
   c.fl.clear();
   c.nn.clear();
+  c.hnn.clear();
+  c.h2_built = false;
+  c.h2pool.reset();
   c.built = c.factored = false;
   c.n = n;
   c.d = d;
@@ -1478,7 +1763,7 @@ int aifmm_factor(void) {
   c.factored = true;
   c.stats[AIFMM_STAT_FACTOR_MS] = ms_since(t0);
   c.stats[AIFMM_STAT_DEVICE_BYTES] =
-      (double)(c.persist.total() + c.scratch0.total() + c.scratch1.total() + c.work.total() + c.buildp.total());
+      (double)chunk_cache().total();
   CAPI_END
 }
 
@@ -1524,7 +1809,12 @@ void aifmm_free(void) {
   if (c.s) cudaStreamSynchronize(c.s);
   c.fl.clear();
   c.nn.clear();
-  // device memory stays cached in the pools (released at process exit or by a failing build)
+  c.hnn.clear();
+  c.h2_built = false;
+  c.h2pool.reset();
+  c.h2work.reset();
+  c.gmpool.reset();
+  // device memory stays cached in the chunk cache (released at process exit or under pressure)
   c.persist.recycle();
   c.scratch0.recycle();
   c.scratch1.recycle();
@@ -1640,6 +1930,43 @@ int aifmm_debug_inverse(double* A, int n, int lda) {
   int info = d2h(c, dinfo, 1)[0];
   c.work.reset();
   if (info) throw Error(AIFMM_ESINGULAR_PIVOT, "singular matrix");
+  CAPI_END
+}
+
+int aifmm_matvec_build(double tol) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built, AIFMM_ESTATE, "matvec_build before build");
+  AIFMM_REQUIRE(tol > 0.0 && tol < 1.0, AIFMM_EINVALID_ARG, "tol must lie in (0,1)");
+  c.h2_built = false;
+  c.h2pool.reset();
+  build_nnca(c, c.hnn, tol / 100.0, c.h2pool);   // reading R18: eps_ACA = tol / 100
+  c.h2_tol = tol;
+  c.h2_built = true;
+  CAPI_END
+}
+
+int aifmm_matvec(const double* X, double* Y, int nrhs) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.h2_built, AIFMM_ESTATE, "matvec before matvec_build");
+  AIFMM_REQUIRE(X && Y && nrhs >= 1, AIFMM_EINVALID_ARG, "bad matvec arguments");
+  matvec_dev(c, X, Y, nrhs);
+  CAPI_END
+}
+
+int aifmm_gmres(const double* b, double* x, int restart, double rtol, int maxit, int precond, int* iters,
+                double* relres) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.h2_built, AIFMM_ESTATE, "gmres before matvec_build");
+  AIFMM_REQUIRE(!precond || c.factored, AIFMM_ESTATE, "preconditioned gmres before factor");
+  AIFMM_REQUIRE(b && x && iters && relres && restart >= 1 && maxit >= 1 && rtol > 0.0, AIFMM_EINVALID_ARG,
+                "bad gmres arguments");
+  AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
+  LAUNCH(finite_kernel, gsz(c.n), 256, 0, c.s, b, c.n, c.dflag);
+  check_flag(c, AIFMM_ENONFINITE, "non-finite right-hand side");
+  gmres_dev(c, b, x, restart, rtol, maxit, precond, iters, relres);
   CAPI_END
 }
 

@@ -118,6 +118,15 @@ struct PqrTask {
   int* t_taken;         // columns appended
 };
 
+// Cholesky G = R^T R of a k x k SPD block (ld k) and R^{-1}; info = 1 + failing step or 0.
+struct CholTask {
+  const double* G;
+  double* R;
+  double* Rinv;
+  int k, pad;
+  int* info;
+};
+
 // Frobenius norm of a column-major block (written to *out).
 struct NormTask {
   const double* A;

@@ -11,6 +11,7 @@
 //   keval_tasks_kernel : kernel-entry blocks A(rows, cols).
 //   copy/norm kernels  : block assembly, level transition gathers, Frobenius norms.
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
@@ -448,6 +449,98 @@ __global__ void gj_unscramble_kernel(const GJBTask* __restrict__ tasks) {
   }
 }
 
+// ------------------------------------------------------------------------------ Cholesky
+// Batched Cholesky G = R^T R (R upper) and the triangular inverse R^{-1}, for CholeskyQR2
+// orthonormalisation of the NNCA bases (reading R13: any orthonormal basis of the same range
+// gives the same exact change of variables).  One CTA per matrix, in shared memory up to
+// CHOL_SMEM_MAX, else in global memory (in place).  info = 1 + step of a non-positive pivot.
+constexpr int CHOL_NT = 256;
+__device__ int chol_inv_device(double* S, int ld, int k, double* tmp) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  // right-looking upper Cholesky: row j of R = (row j of the trailing G) / sqrt(pivot)
+  for (int j = 0; j < k; ++j) {
+    const double piv = S[(size_t)j * ld + j];
+    if (!(piv > 0.0)) {
+      if (tid == 0) bad = j + 1;
+      __syncthreads();
+      return bad;
+    }
+    const double d = sqrt(piv);
+    __syncthreads();
+    for (int c = j + 1 + tid; c < k; c += CHOL_NT) S[(size_t)c * ld + j] /= d;
+    __syncthreads();
+    if (tid == 0) S[(size_t)j * ld + j] = d;
+    // trailing update of the upper triangle: G[r, c] -= R[j, r] R[j, c], r <= c
+    for (int c = j + 1 + warp; c < k; c += CHOL_NT / 32) {
+      const double rc = S[(size_t)c * ld + j];
+      for (int r = j + 1 + lane; r <= c; r += 32) S[(size_t)c * ld + r] -= S[(size_t)r * ld + j] * rc;
+    }
+    __syncthreads();
+  }
+  // zero the strict lower triangle (R is upper)
+  for (int c = warp; c < k; c += CHOL_NT / 32)
+    for (int r = c + 1 + lane; r < k; r += 32) S[(size_t)c * ld + r] = 0.0;
+  __syncthreads();
+  return 0;
+}
+// in-place inverse of an upper-triangular matrix (column by column, dtrti2 order)
+__device__ void trtri_upper_device(double* S, int ld, int k, double* tmp) {
+  const int tid = threadIdx.x;
+  for (int j = 0; j < k; ++j) {
+    const double ajj = 1.0 / S[(size_t)j * ld + j];
+    for (int i = tid; i < j; i += CHOL_NT) tmp[i] = S[(size_t)j * ld + i];
+    __syncthreads();
+    // column j (rows < j) = -ajj * Rinv[0:j, 0:j] * R[0:j, j]
+    for (int i = tid; i < j; i += CHOL_NT) {
+      double s = 0.0;
+      for (int l = i; l < j; ++l) s += S[(size_t)l * ld + i] * tmp[l];
+      S[(size_t)j * ld + i] = -ajj * s;
+    }
+    __syncthreads();
+    if (tid == 0) S[(size_t)j * ld + j] = ajj;
+    __syncthreads();
+  }
+}
+constexpr int CHOL_SMEM_MAX = 160;
+__global__ void __launch_bounds__(CHOL_NT) chol_inv_kernel(const CholTask* __restrict__ tasks, int smem_doubles) {
+  extern __shared__ double csm[];
+  const CholTask tk = tasks[blockIdx.x];
+  const int k = tk.k;
+  if (k == 0) { if (threadIdx.x == 0) *tk.info = 0; return; }
+  const bool smem = (long long)k * (k + 1) <= smem_doubles;
+  double* S = smem ? csm : tk.Rinv;
+  double* tmp = smem ? csm + (size_t)k * k : tk.R;   // global path: R's storage is the temp until the end
+  for (int c = 0; c < k; ++c)
+    for (int r = threadIdx.x; r < k; r += CHOL_NT) S[(size_t)c * k + r] = tk.G[(size_t)c * k + r];
+  __syncthreads();
+  const int info = chol_inv_device(S, k, k, tmp);
+  if (threadIdx.x == 0) *tk.info = info;
+  if (info) return;
+  if (smem) {
+    for (int c = 0; c < k; ++c)
+      for (int r = threadIdx.x; r < k; r += CHOL_NT) tk.R[(size_t)c * k + r] = S[(size_t)c * k + r];
+    __syncthreads();
+    trtri_upper_device(S, k, k, tmp);
+    for (int c = 0; c < k; ++c)
+      for (int r = threadIdx.x; r < k; r += CHOL_NT) tk.Rinv[(size_t)c * k + r] = S[(size_t)c * k + r];
+  } else {
+    // R is in Rinv's storage: copy it out, then invert in place using a column of dynamic smem
+    for (int c = 0; c < k; ++c)
+      for (int r = threadIdx.x; r < k; r += CHOL_NT) tk.R[(size_t)c * k + r] = S[(size_t)c * k + r];
+    __syncthreads();
+    trtri_upper_device(S, k, k, csm);
+  }
+}
+void launch_chol_inv(const CholTask* t, int ntasks, int kmax, cudaStream_t s) {
+  const int kk = std::min(kmax, CHOL_SMEM_MAX);
+  const int nd = std::max(kk * (kk + 1), kmax);   // global-path tasks need k doubles of temp
+  ensure_dyn_smem(chol_inv_kernel, (size_t)nd * sizeof(double));
+  LAUNCH(chol_inv_kernel, ntasks, CHOL_NT, (size_t)nd * sizeof(double), s, t, nd);
+}
+
 // ------------------------------------------------------------------------------ pivoted QR
 constexpr int PQR_NT = 256;
 constexpr double TIE = 1e-10;  // reading R7 (same rule as oracle/linalg.py: pick)
@@ -741,7 +834,10 @@ struct HHTask {
   double* T;     // workspace HHB x HHB (ld HHB)
 };
 
-__global__ void __launch_bounds__(256) hh_panel_kernel(const HHTask* __restrict__ tasks, int j) {
+// One CTA (512 threads) per task, panel read from global memory / L2: used when the batch
+// has enough tasks to fill the GPU (the cluster variants below spread one task over 8 SMs).
+constexpr int HHP_NT = 512;
+__global__ void __launch_bounds__(HHP_NT) hh_panel_kernel(const HHTask* __restrict__ tasks, int j) {
   const HHTask tk = tasks[blockIdx.x];
   const int r = min(tk.n, tk.m);
   if (j >= r) return;
@@ -750,13 +846,15 @@ __global__ void __launch_bounds__(256) hh_panel_kernel(const HHTask* __restrict_
   __shared__ double red[32];
   __shared__ double tau_s[HHB];
   __shared__ double G[HHB][HHB + 1];
+  __shared__ double Ts[HHB][HHB + 1];
+  constexpr int NW = HHP_NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int c = 0; c < nbw; ++c) {
     double* x = A + (size_t)c * ld + c;     // column c, from the diagonal down
     const int len = rows - c;
     double p = 0.0;
-    for (int i = 1 + tid; i < len; i += 256) p += x[i] * x[i];
-    const double sigma = block_sum<256>(p, red);
+    for (int i = 1 + tid; i < len; i += HHP_NT) p += x[i] * x[i];
+    const double sigma = block_sum<HHP_NT>(p, red);
     const double alpha = x[0];
     double tau = 0.0, beta = alpha, scal = 0.0;
     if (sigma > 0.0) {
@@ -767,11 +865,11 @@ __global__ void __launch_bounds__(256) hh_panel_kernel(const HHTask* __restrict_
     }
     // v = [1; x[1:] * scal], A[c][c] = beta
     if (sigma > 0.0)
-      for (int i = 1 + tid; i < len; i += 256) x[i] *= scal;
+      for (int i = 1 + tid; i < len; i += HHP_NT) x[i] *= scal;
     __syncthreads();
     if (tid == 0) { x[0] = beta; tau_s[c] = tau; }
     // apply H = I - tau v v^T to the remaining panel columns (one warp per column)
-    for (int cc = c + 1 + warp; cc < nbw; cc += 8) {
+    for (int cc = c + 1 + warp; cc < nbw; cc += NW) {
       double* y = A + (size_t)cc * ld + c;
       double w = (lane == 0) ? y[0] : 0.0;
       for (int i = 1 + lane; i < len; i += 32) w += x[i] * y[i];
@@ -783,36 +881,38 @@ __global__ void __launch_bounds__(256) hh_panel_kernel(const HHTask* __restrict_
     __syncthreads();
   }
   // explicit V (rows j..n of the full matrix, ld n): unit diagonal, zeros above
-  for (int e = tid; e < rows * nbw; e += 256) {
-    const int i = e % rows, c = e / rows;
-    double v = (i < c) ? 0.0 : (i == c ? 1.0 : A[(size_t)c * ld + i]);
-    tk.V[(size_t)c * tk.n + i] = v;
+  for (int c = warp; c < nbw; c += NW) {
+    const double* src = A + (size_t)c * ld;
+    double* dst = tk.V + (size_t)c * tk.n;
+    for (int i = lane; i < rows; i += 32) dst[i] = (i < c) ? 0.0 : (i == c ? 1.0 : src[i]);
   }
   __syncthreads();
-  // Gram V^T V (nbw x nbw), one warp per entry
-  for (int e = warp; e < nbw * nbw; e += 8) {
+  // Gram V^T V (a < b), one warp per entry
+  for (int e = warp; e < nbw * nbw; e += NW) {
     const int a = e % nbw, b = e / nbw;
-    if (a >= b) continue;     // only a < b needed
+    if (a >= b) continue;
+    const double* va = tk.V + (size_t)a * tk.n;
+    const double* vb = tk.V + (size_t)b * tk.n;
     double s = 0.0;
-    for (int i = lane; i < rows; i += 32) s += tk.V[(size_t)a * tk.n + i] * tk.V[(size_t)b * tk.n + i];
+    for (int i = b + lane; i < rows; i += 32) s += va[i] * vb[i];   // v_b is zero above row b
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) G[a][b] = s;
   }
+  for (int e = tid; e < HHB * HHB; e += HHP_NT) Ts[e % HHB][e / HHB] = 0.0;
   __syncthreads();
-  if (tid == 0) {
-    // dlarft (forward, columnwise): T[0:i, i] = -tau_i T[0:i, 0:i] (V^T v_i)
-    double* T = tk.T;
-    for (int e = 0; e < HHB * HHB; ++e) T[e] = 0.0;
-    for (int i = 0; i < nbw; ++i) {
-      const double ti = tau_s[i];
-      T[i + i * HHB] = ti;
-      for (int a = 0; a < i; ++a) {
-        double s = 0.0;
-        for (int b = a; b < i; ++b) s += T[a + b * HHB] * G[b][i];
-        T[a + i * HHB] = -ti * s;
-      }
+  // dlarft (forward, columnwise): T[0:i, i] = -tau_i T[0:i, 0:i] (V^T v_i), rows in parallel
+  for (int i = 0; i < nbw; ++i) {
+    const double ti = tau_s[i];
+    if (tid < i) {
+      double s = 0.0;
+      for (int b = tid; b < i; ++b) s += Ts[tid][b] * G[b][i];
+      Ts[tid][i] = -ti * s;
+    } else if (tid == i) {
+      Ts[i][i] = ti;
     }
+    __syncthreads();
   }
+  for (int e = tid; e < HHB * HHB; e += HHP_NT) tk.T[e] = Ts[e % HHB][e / HHB];
 }
 
 // Cluster variant of the panel: the 8 CTAs of a cluster split the panel rows and combine
@@ -1045,6 +1145,124 @@ hh_panel_cluster_smem_kernel(const HHTask* __restrict__ tasks, int j, int cap_ro
   cl.sync();
 }
 
+// Fused trailing update of one Householder panel (compact WY, forward): for a 64-column block
+// C of the trailing matrix (rows j..n, all of them), C <- (I - V T V^T)^T C = C - V (T^T (V^T C)).
+// One CTA per (task, column block); both passes over C stream rows in 32-row chunks staged in
+// shared memory, the products run on DMMA (mma.sync m8n8k4 f64).  Fixed summation order.
+struct HHUTile { int task, n0; };
+constexpr int HHU_NT = 256;
+constexpr int HHU_BN = 64, HHU_RK = 32;   // column block, row chunk
+__global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restrict__ tasks,
+                                                           const HHUTile* __restrict__ tiles, int j) {
+  const HHUTile tl = tiles[blockIdx.x];
+  const HHTask tk = tasks[tl.task];
+  const int r = min(tk.n, tk.m);
+  const int nbw = min(HHB, r - j), rows = tk.n - j, ld = tk.lda;
+  const int nc = tk.m - j - nbw;
+  const int n0 = tl.n0, ncb = min(HHU_BN, nc - n0);
+  double* C = tk.A + j + (size_t)(j + nbw + n0) * ld;
+  const double* V = tk.V;
+  __shared__ __align__(16) double Vs[HHU_RK][HHB + 4];
+  __shared__ __align__(16) double Cs[HHU_RK][HHU_BN + 4];
+  __shared__ __align__(16) double Zs[HHB][HHU_BN + 4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;   // 2 x 4 warps over 32 x 64
+  const double* __restrict__ Tg = tk.T;                     // HHB x HHB, ld HHB (L1-resident)
+  auto load_chunk = [&](int r0) {
+    for (int e = tid; e < HHU_RK * HHB; e += HHU_NT) {
+      const int rr = e % HHU_RK, c = e / HHU_RK, gr = r0 + rr;
+      Vs[rr][c] = (gr < rows && c < nbw) ? V[(size_t)c * tk.n + gr] : 0.0;
+    }
+    for (int e = tid; e < HHU_RK * HHU_BN; e += HHU_NT) {
+      const int rr = e % HHU_RK, c = e / HHU_RK, gr = r0 + rr;
+      Cs[rr][c] = (gr < rows && c < ncb) ? C[(size_t)c * ld + gr] : 0.0;
+    }
+  };
+  // pass 1: Z = V^T C  (32 x 64, K = rows)
+  double acc[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+  for (int r0 = 0; r0 < rows; r0 += HHU_RK) {
+    __syncthreads();
+    load_chunk(r0);
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < HHU_RK; kk += 4) {
+      double a[2], b[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = Vs[kk + (lane & 3)][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) b[q] = Cs[kk + (lane & 3)][wn + q * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) dmma_884(acc[i][q][0], acc[i][q][1], a[i], b[q]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) Zs[wm + i * 8 + (lane >> 2)][wn + q * 8 + (lane & 3) * 2 + e] = acc[i][q][e];
+  __syncthreads();
+  // Z2 = T^T Z (rows >= nbw vanish because T is zero there)
+  double z2[HHB * HHU_BN / HHU_NT];
+#pragma unroll
+  for (int t = 0; t < HHB * HHU_BN / HHU_NT; ++t) {
+    const int e = tid + t * HHU_NT, i = e % HHB, c = e / HHB;
+    double s = 0.0;
+    for (int a2 = 0; a2 <= i; ++a2) s += __ldg(Tg + a2 + i * HHB) * Zs[a2][c];   // T upper triangular
+    z2[t] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < HHB * HHU_BN / HHU_NT; ++t) {
+    const int e = tid + t * HHU_NT, i = e % HHB, c = e / HHB;
+    Zs[i][c] = z2[t];
+  }
+  // pass 2: C -= V Z2, chunk by chunk
+  for (int r0 = 0; r0 < rows; r0 += HHU_RK) {
+    __syncthreads();
+    load_chunk(r0);
+    __syncthreads();
+    double o[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) o[i][q][0] = o[i][q][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < HHB; kk += 4) {
+      double a[2], b[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = Vs[wm + i * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) b[q] = Zs[kk + (lane & 3)][wn + q * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) dmma_884(o[i][q][0], o[i][q][1], a[i], b[q]);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) Cs[wm + i * 8 + (lane >> 2)][wn + q * 8 + (lane & 3) * 2 + e] -= o[i][q][e];
+    __syncthreads();
+    for (int e = tid; e < HHU_RK * HHU_BN; e += HHU_NT) {
+      const int rr = e % HHU_RK, c = e / HHU_RK, gr = r0 + rr;
+      if (gr < rows && c < ncb) C[(size_t)c * ld + gr] = Cs[rr][c];
+    }
+  }
+}
+void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s) {
+  LAUNCH(hh_update_kernel, ntiles, HHU_NT, 0, s, static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j);
+}
+
 // M = R^T (m x r) from the upper triangle of the factored A (n x m, lda)
 __global__ void hh_extract_rt_kernel(const HHTask* __restrict__ tasks, double* const* __restrict__ out, const int* ldo) {
   const HHTask tk = tasks[blockIdx.x];
@@ -1191,7 +1409,7 @@ void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode,
   } else if (mode == 1) {
     LAUNCH(hh_panel_cluster_kernel, ntasks * HHC, 256, 0, s, static_cast<const HHTask*>(t), j);
   } else {
-    LAUNCH(hh_panel_kernel, ntasks, 256, 0, s, static_cast<const HHTask*>(t), j);
+    LAUNCH(hh_panel_kernel, ntasks, HHP_NT, 0, s, static_cast<const HHTask*>(t), j);
   }
 }
 void launch_hh_extract(const void* t, int ntasks, double* const* out, const int* ldo, cudaStream_t s) {

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <string>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <set>
 #include <unordered_map>
@@ -22,6 +23,7 @@ void launch_pqr_cluster(const PqrTask* t, int ntasks, cudaStream_t s);
 void launch_keval(const KEvalTask* t, int ntasks, int ysplit, const double* pts, KernelParams kp, int* flag, cudaStream_t s);
 void launch_copy(const CopyTask* t, int ntasks, int ysplit, cudaStream_t s);
 void launch_norm(const NormTask* t, int ntasks, cudaStream_t s);
+void launch_chol_inv(const CholTask* t, int ntasks, int kmax, cudaStream_t s);
 void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s);
 void launch_gj_unscramble(const void* t, int ntasks, cudaStream_t s);
 size_t gjb_task_size();
@@ -30,6 +32,7 @@ size_t hh_task_size();
 void hh_make(void* out, double* A, int lda, int n, int m, double* V, double* T);
 void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode, int nmax);
 void launch_hh_extract(const void* t, int ntasks, double* const* out, const int* ldo, cudaStream_t s);
+void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s);
 constexpr int HH_PANEL = 32;
 constexpr int GJ_SMALL_MAX = 160;  // in-place inverses up to this size run in shared memory (<= 206 KB)
 constexpr int GJ_PANEL = 32;
@@ -47,6 +50,15 @@ struct Prof {
     cudaStreamSynchronize(s);
     ms[name] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
+  // host-only lap timer (no stream synchronisation): accumulates under "h.<name>"
+  std::chrono::steady_clock::time_point hl;
+  void hstart() { if (on) hl = std::chrono::steady_clock::now(); }
+  void hlap(const char* name) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    ms[std::string("h.") + name] += std::chrono::duration<double, std::milli>(t - hl).count();
+    hl = t;
+  }
   void dump(const char* title) {
     if (!on) return;
     fprintf(stderr, "[aifmm profile] %s:", title);
@@ -58,99 +70,117 @@ struct Prof {
 inline Prof g_prof;
 
 // ---------------------------------------------------------------------------------- pools
-// Chunked bump allocator of device memory.  Blocks live until reset()/release().  Chunks are
-// cached across reset() (so repeated build/factor cycles stay out of cudaMalloc/cudaFree);
-// under memory pressure every registered pool gives back its chunks that hold no live block
-// (trim) and the allocation is retried once.
-class DevPool;
-inline std::vector<DevPool*>& pool_registry() {
-  static std::vector<DevPool*> r;
-  return r;
+// Device memory: one process-wide cache of fixed-size chunks (oversize requests get a
+// dedicated chunk) shared by every pool, so the per-level pools hand chunks to each other
+// instead of going through cudaMalloc/cudaFree; under memory pressure the cache gives its
+// idle chunks back and the allocation is retried once.  All work runs on one stream, so a
+// chunk returned by reset() can be handed out again at once (stream order).
+class ChunkCache {
+ public:
+  static constexpr size_t CH = (size_t)512 << 20;
+  void* get(size_t bytes, size_t* got) {
+    if (bytes <= CH) {
+      *got = CH;
+      if (!free_.empty()) {
+        void* p = free_.back();
+        free_.pop_back();
+        return p;
+      }
+      return fresh(CH);
+    }
+    // oversize: best fit among the idle oversize chunks
+    size_t best = (size_t)-1;
+    for (size_t i = 0; i < big_.size(); ++i)
+      if (big_[i].second >= bytes && (best == (size_t)-1 || big_[i].second < big_[best].second)) best = i;
+    if (best != (size_t)-1 && big_[best].second <= 2 * bytes) {
+      auto r = big_[best];
+      big_.erase(big_.begin() + best);
+      *got = r.second;
+      return r.first;
+    }
+    const size_t sz = (bytes + CH - 1) / CH * CH;
+    *got = sz;
+    return fresh(sz);
+  }
+  void put(void* p, size_t sz) {
+    if (sz == CH) free_.push_back(p);
+    else big_.push_back({p, sz});
+  }
+  // give every idle chunk back to the driver
+  void trim() {
+    if (free_.empty() && big_.empty()) return;
+    cudaDeviceSynchronize();
+    for (void* p : free_) { cudaFree(p); total_ -= CH; }
+    for (auto& b : big_) { cudaFree(b.first); total_ -= b.second; }
+    free_.clear();
+    big_.clear();
+  }
+  size_t total() const { return total_; }
+  size_t idle() const {
+    size_t t = free_.size() * CH;
+    for (auto& b : big_) t += b.second;
+    return t;
+  }
+
+ private:
+  void* fresh(size_t sz) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      trim();
+      e = cudaMalloc(&p, sz);
+    }
+    AIFMM_CUDA(e);
+    total_ += sz;
+    return p;
+  }
+  std::vector<void*> free_;
+  std::vector<std::pair<void*, size_t>> big_;
+  size_t total_ = 0;
+};
+inline ChunkCache& chunk_cache() {
+  static ChunkCache* c = new ChunkCache();   // never destroyed: chunks die with the context
+  return *c;
 }
+
+// Bump allocator over chunks of the cache.  Blocks live until reset() returns the chunks.
 class DevPool {
  public:
-  explicit DevPool(size_t chunk = (size_t)256 << 20) : chunk_(chunk) { pool_registry().push_back(this); }
-  ~DevPool() {
-    release();
-    auto& r = pool_registry();
-    r.erase(std::remove(r.begin(), r.end(), this), r.end());
-  }
+  explicit DevPool(size_t = 0) {}
+  ~DevPool() { reset(); }
   DevPool(const DevPool&) = delete;
   DevPool& operator=(const DevPool&) = delete;
   void* alloc(size_t bytes) {
     bytes = (bytes + 255) & ~(size_t)255;
     if (bytes == 0) bytes = 256;
-    if (cur_ < chunks_.size() && used_ + bytes <= sizes_[cur_]) {
-      void* p = static_cast<char*>(chunks_[cur_]) + used_;
+    if (!chunks_.empty() && used_ + bytes <= chunks_.back().second) {
+      void* p = static_cast<char*>(chunks_.back().first) + used_;
       used_ += bytes;
       return p;
     }
-    // next existing chunk large enough, else a new one
-    for (size_t c = cur_ + 1; c < chunks_.size(); ++c) {
-      if (bytes <= sizes_[c]) {
-        cur_ = c;
-        used_ = bytes;
-        return chunks_[c];
-      }
-    }
-    size_t sz = std::max(chunk_, bytes);
-    void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, sz);
-    if (e == cudaErrorMemoryAllocation) {
-      cudaGetLastError();
-      for (DevPool* q : pool_registry()) q->trim();
-      e = cudaMalloc(&p, sz);
-    }
-    AIFMM_CUDA(e);
-    // keep the chunk list ordered by use: a new chunk goes right after the current one
-    const size_t at = chunks_.empty() ? 0 : cur_ + 1;
-    chunks_.insert(chunks_.begin() + at, p);
-    sizes_.insert(sizes_.begin() + at, sz);
-    total_ += sz;
-    cur_ = at;
+    size_t got = 0;
+    void* p = chunk_cache().get(bytes, &got);
+    chunks_.push_back({p, got});
+    held_ += got;
     used_ = bytes;
     return p;
   }
   double* d(size_t n) { return static_cast<double*>(alloc(n * sizeof(double))); }
   int* i(size_t n) { return static_cast<int*>(alloc(n * sizeof(int))); }
-  void reset() { cur_ = 0; used_ = 0; }
-  // recycle: forget every allocation but keep the chunks cached for the next build (a caching
-  // allocator: cudaMalloc/cudaFree stay out of repeated build/factor cycles)
-  void recycle() { reset(); }
-  // give back the cached chunks that hold no live block (those after the current one)
-  void trim() {
-    if (chunks_.empty()) return;
-    const size_t keep = (used_ == 0 && cur_ == 0) ? 0 : cur_ + 1;
-    if (keep < chunks_.size()) cudaDeviceSynchronize();
-    for (size_t c = keep; c < chunks_.size(); ++c) {
-      cudaFree(chunks_[c]);
-      total_ -= sizes_[c];
-    }
-    chunks_.resize(keep);
-    sizes_.resize(keep);
-    if (keep == 0) { cur_ = 0; used_ = 0; }
-  }
-  void release() {
-    if (!chunks_.empty()) cudaDeviceSynchronize();
-    for (void* p : chunks_) cudaFree(p);
+  // return every chunk to the cache (the blocks are dead; stream order makes reuse safe)
+  void reset() {
+    for (auto& c : chunks_) chunk_cache().put(c.first, c.second);
     chunks_.clear();
-    sizes_.clear();
-    cur_ = 0;
     used_ = 0;
-    total_ = 0;
+    held_ = 0;
   }
-  size_t total() const { return total_; }
-  size_t in_use() const {
-    size_t u = used_;
-    for (size_t c = 0; c < cur_ && c < sizes_.size(); ++c) u += sizes_[c];
-    return u;
-  }
+  void recycle() { reset(); }
+  size_t total() const { return held_; }
 
  private:
-  size_t chunk_;
-  std::vector<void*> chunks_;
-  std::vector<size_t> sizes_;
-  size_t cur_ = 0, used_ = 0, total_ = 0;
+  std::vector<std::pair<void*, size_t>> chunks_;
+  size_t used_ = 0, held_ = 0;
 };
 
 // Pinned host staging + device mirror for task arrays.  An append is copied H2D at once;
@@ -439,15 +469,19 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
   // very long panels (cluster, global memory)
   const int SM_ROWS = 8 * ((176 * 1024) / (HH_PANEL * 8));
   std::vector<TriRootReq> sorted_reqs;
-  for (const auto& q : reqs) if (q.n < 512) sorted_reqs.push_back(q);
+  // enough tasks to fill the GPU with one CTA each: no clusters (their 8x more CTAs only add
+  // waves of latency-bound panel steps)
+  static const bool hh_cluster = getenv("AIFMM_HH_CLUSTER") != nullptr;   // debug toggle
+  const bool many = !hh_cluster && reqs.size() >= 2 * 148;
+  for (const auto& q : reqs) if (q.n < 512 || many) sorted_reqs.push_back(q);
   const size_t nsmall = sorted_reqs.size();
   int nmax_mid = 0;
-  for (const auto& q : reqs) if (q.n >= 512 && q.n <= SM_ROWS) { sorted_reqs.push_back(q); nmax_mid = std::max(nmax_mid, q.n); }
+  for (const auto& q : reqs) if (!many && q.n >= 512 && q.n <= SM_ROWS) { sorted_reqs.push_back(q); nmax_mid = std::max(nmax_mid, q.n); }
   const size_t nmid = sorted_reqs.size() - nsmall;
-  for (const auto& q : reqs) if (q.n > SM_ROWS) sorted_reqs.push_back(q);
+  for (const auto& q : reqs) if (!many && q.n > SM_ROWS) sorted_reqs.push_back(q);
   const std::vector<TriRootReq>& R = sorted_reqs;
   std::vector<char> tb(tsz * reqs.size());
-  std::vector<double*> V(reqs.size()), T(reqs.size()), Z(reqs.size()), Z2(reqs.size());
+  std::vector<double*> V(reqs.size()), T(reqs.size());
   std::vector<double*> outs(reqs.size());
   std::vector<int> ldo(reqs.size());
   int rmax = 0;
@@ -455,8 +489,6 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
     const TriRootReq& q = R[i];
     V[i] = work.d((size_t)std::max(q.n, 1) * HH_PANEL);
     T[i] = work.d((size_t)HH_PANEL * HH_PANEL);
-    Z[i] = work.d((size_t)HH_PANEL * std::max(q.m, 1));
-    Z2[i] = work.d((size_t)HH_PANEL * std::max(q.m, 1));
     hh_make(tb.data() + i * tsz, q.A, q.lda, q.n, q.m, V[i], T[i]);
     outs[i] = q.out;
     ldo[i] = q.ldm;
@@ -474,27 +506,18 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
     if (nmid) launch_hh_panel(static_cast<const char*>(dt) + nsmall * tsz, (int)nmid, j, s, 2, nmax_mid);
     if (reqs.size() > nsmall + nmid)
       launch_hh_panel(static_cast<const char*>(dt) + (nsmall + nmid) * tsz, (int)(reqs.size() - nsmall - nmid), j, s, 1, 0);
-    GemmBatch g1, g2, g3;
-    g1.set_splitk_pool(&work);
+    // fused trailing update: one CTA per (task, 64-column block of the trailing matrix)
+    std::vector<int2> ut;
     for (size_t i = 0; i < reqs.size(); ++i) {
       const TriRootReq& q = R[i];
       const int r = std::min(q.n, q.m);
       if (j >= r) continue;
       const int nbw = std::min(HH_PANEL, r - j);
       const int nc = q.m - j - nbw;
-      if (nc <= 0) continue;
-      double* C = q.A + j + (size_t)(j + nbw) * q.lda;
-      g1.task(Z[i], HH_PANEL, nbw, nc, 0.0);
-      g1.term(1.0, V[i], q.n, 1, C, q.lda, 0, q.n - j);
-      g2.task(Z2[i], HH_PANEL, nbw, nc, 0.0);
-      g2.term(1.0, T[i], HH_PANEL, 1, Z[i], HH_PANEL, 0, nbw);
-      g3.task(C, q.lda, q.n - j, nc, 1.0);
-      g3.term(-1.0, V[i], q.n, 0, Z2[i], HH_PANEL, 0, nbw);
+      for (int n0 = 0; n0 < nc; n0 += 64) ut.push_back(make_int2((int)i, n0));
     }
     if (g_prof.on) { g_prof.end("hh.panel"); g_prof.begin(s); }
-    g1.run(up, s);
-    g2.run(up, s);
-    g3.run(up, s);
+    if (!ut.empty()) launch_hh_update(dt, up.put(ut), (int)ut.size(), j, s);
     if (g_prof.on) g_prof.end("hh.trail");
   }
   if (g_prof.on) g_prof.begin(s);
@@ -504,8 +527,10 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
 inline void run_pqr(const std::vector<PqrTask>& v, Uploader& up, cudaStream_t s) {
   std::vector<PqrTask> small, big;
   size_t smem = 0;
+  // many tasks: one CTA each fills the GPU; few tall tasks: 8-CTA clusters
+  const bool many = v.size() >= 2 * 148;
   for (const PqrTask& t : v) {
-    if (t.m >= 128) big.push_back(t);
+    if (t.m >= 128 && !many) big.push_back(t);
     else {
       small.push_back(t);
       smem = std::max(smem, (size_t)t.ncols + t.m + t.k0 + t.tmax + 8);
