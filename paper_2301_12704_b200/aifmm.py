@@ -104,7 +104,9 @@ def solve(B):
     lib = load()
     one = B.dim() == 1
     Bm = B[:, None] if one else B
-    Bc = Bm.to(torch.float64).t().contiguous()        # (nrhs, n) row-major == (n, nrhs) column-major
+    # (nrhs, n) row-major == (n, nrhs) column-major; always a fresh buffer (the library solves in
+    # place, and for one column .t().contiguous() would alias the caller's tensor)
+    Bc = Bm.to(torch.float64).t().contiguous().clone()
     _check(lib.aifmm_solve(ctypes.c_void_p(Bc.data_ptr()), Bc.shape[0]))
     X = Bc.t()
     return X[:, 0] if one else X

@@ -549,10 +549,13 @@ static void setup_level(Ctx& c, int l) {
   // contiguous within a chunk, so the memset runs over few ranges
   auto rnd = [](size_t x) { return (std::max<size_t>(x * 8, 1) + 255) & ~(size_t)255; };
   std::vector<std::pair<char*, size_t>> zr;
+  size_t zchunk = (size_t)-1;
   auto carve = [&](size_t nel) {
     char* p = static_cast<char*>(S.alloc(rnd(nel)));
-    if (!zr.empty() && zr.back().first + zr.back().second == p) zr.back().second += rnd(nel);
+    // merge only within one chunk (separate allocations may be adjacent in address space)
+    if (!zr.empty() && S.nchunks() == zchunk && zr.back().first + zr.back().second == p) zr.back().second += rnd(nel);
     else zr.push_back({p, rnd(nel)});
+    zchunk = S.nchunks();
     return reinterpret_cast<double*>(p);
   };
   for (int b : f.boxes) {

@@ -1151,9 +1151,12 @@ hh_panel_cluster_smem_kernel(const HHTask* __restrict__ tasks, int j, int cap_ro
 // shared memory, the products run on DMMA (mma.sync m8n8k4 f64).  Fixed summation order.
 struct HHUTile { int task, n0; };
 constexpr int HHU_NT = 256;
-constexpr int HHU_BN = 64, HHU_RK = 32;   // column block, row chunk
+constexpr int HHU_BN = 64, HHU_RK = 32, HHU_ST = 3;   // column block, row chunk, pipeline stages
+constexpr int HHU_LV = HHB + 4, HHU_LC = HHU_BN + 4;  // padded rows (stride = 4 mod 16: no bank conflicts)
+constexpr size_t HHU_SMEM = sizeof(double) * ((size_t)HHU_ST * HHU_RK * (HHU_LV + HHU_LC) + (size_t)HHB * HHU_LC);
 __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restrict__ tasks,
                                                            const HHUTile* __restrict__ tiles, int j) {
+  extern __shared__ __align__(16) double hhu_smem[];
   const HHUTile tl = tiles[blockIdx.x];
   const HHTask tk = tasks[tl.task];
   const int r = min(tk.n, tk.m);
@@ -1162,52 +1165,65 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
   const int n0 = tl.n0, ncb = min(HHU_BN, nc - n0);
   double* C = tk.A + j + (size_t)(j + nbw + n0) * ld;
   const double* V = tk.V;
-  __shared__ __align__(16) double Vs[HHU_RK][HHB + 4];
-  __shared__ __align__(16) double Cs[HHU_RK][HHU_BN + 4];
-  __shared__ __align__(16) double Zs[HHB][HHU_BN + 4];
+  double* Vs = hhu_smem;                                  // [ST][RK][LV]
+  double* Cs = Vs + (size_t)HHU_ST * HHU_RK * HHU_LV;     // [ST][RK][LC]
+  double* Zs = Cs + (size_t)HHU_ST * HHU_RK * HHU_LC;     // [HHB][LC]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;   // 2 x 4 warps over 32 x 64
   const double* __restrict__ Tg = tk.T;                     // HHB x HHB, ld HHB (L1-resident)
-  auto load_chunk = [&](int r0) {
-    for (int e = tid; e < HHU_RK * HHB; e += HHU_NT) {
-      const int rr = e % HHU_RK, c = e / HHU_RK, gr = r0 + rr;
-      Vs[rr][c] = (gr < rows && c < nbw) ? V[(size_t)c * tk.n + gr] : 0.0;
+  const int nch = (rows + HHU_RK - 1) / HHU_RK;
+  auto issue = [&](int ch) {
+    if (ch < nch) {
+      const int st = ch % HHU_ST, r0 = ch * HHU_RK;
+      double* vs = Vs + (size_t)st * HHU_RK * HHU_LV;
+      double* cs = Cs + (size_t)st * HHU_RK * HHU_LC;
+      for (int e = tid; e < HHU_RK * HHB; e += HHU_NT) {
+        const int rr = e % HHU_RK, c = e / HHU_RK, gr = r0 + rr;
+        const bool ok = gr < rows && c < nbw;
+        cp_async8(vs + rr * HHU_LV + c, ok ? V + (size_t)c * tk.n + gr : V, ok);
+      }
+      for (int e = tid; e < HHU_RK * HHU_BN; e += HHU_NT) {
+        const int rr = e % HHU_RK, c = e / HHU_RK, gr = r0 + rr;
+        const bool ok = gr < rows && c < ncb;
+        cp_async8(cs + rr * HHU_LC + c, ok ? C + (size_t)c * ld + gr : C, ok);
+      }
     }
-    for (int e = tid; e < HHU_RK * HHU_BN; e += HHU_NT) {
-      const int rr = e % HHU_RK, c = e / HHU_RK, gr = r0 + rr;
-      Cs[rr][c] = (gr < rows && c < ncb) ? C[(size_t)c * ld + gr] : 0.0;
-    }
+    cp_async_commit();
   };
-  // pass 1: Z = V^T C  (32 x 64, K = rows)
+  // pass 1: Z = V^T C  (32 x 64, K = rows), 3-stage cp.async pipeline
   double acc[2][2][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int q = 0; q < 2; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
-  for (int r0 = 0; r0 < rows; r0 += HHU_RK) {
+  for (int s = 0; s < HHU_ST - 1; ++s) issue(s);
+  for (int ch = 0; ch < nch; ++ch) {
+    issue(ch + HHU_ST - 1);
+    cp_async_wait<HHU_ST - 1>();
     __syncthreads();
-    load_chunk(r0);
-    __syncthreads();
+    const double* vs = Vs + (size_t)(ch % HHU_ST) * HHU_RK * HHU_LV;
+    const double* cs = Cs + (size_t)(ch % HHU_ST) * HHU_RK * HHU_LC;
 #pragma unroll
     for (int kk = 0; kk < HHU_RK; kk += 4) {
       double a[2], b[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) a[i] = Vs[kk + (lane & 3)][wm + i * 8 + (lane >> 2)];
+      for (int i = 0; i < 2; ++i) a[i] = vs[(kk + (lane & 3)) * HHU_LV + wm + i * 8 + (lane >> 2)];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) b[q] = Cs[kk + (lane & 3)][wn + q * 8 + (lane >> 2)];
+      for (int q = 0; q < 2; ++q) b[q] = cs[(kk + (lane & 3)) * HHU_LC + wn + q * 8 + (lane >> 2)];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int q = 0; q < 2; ++q) dmma_884(acc[i][q][0], acc[i][q][1], a[i], b[q]);
     }
+    __syncthreads();
   }
-  __syncthreads();
+  cp_async_wait<0>();
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int q = 0; q < 2; ++q)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) Zs[wm + i * 8 + (lane >> 2)][wn + q * 8 + (lane & 3) * 2 + e] = acc[i][q][e];
+      for (int e = 0; e < 2; ++e) Zs[(wm + i * 8 + (lane >> 2)) * HHU_LC + wn + q * 8 + (lane & 3) * 2 + e] = acc[i][q][e];
   __syncthreads();
   // Z2 = T^T Z (rows >= nbw vanish because T is zero there)
   double z2[HHB * HHU_BN / HHU_NT];
@@ -1215,20 +1231,24 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
   for (int t = 0; t < HHB * HHU_BN / HHU_NT; ++t) {
     const int e = tid + t * HHU_NT, i = e % HHB, c = e / HHB;
     double s = 0.0;
-    for (int a2 = 0; a2 <= i; ++a2) s += __ldg(Tg + a2 + i * HHB) * Zs[a2][c];   // T upper triangular
+    for (int a2 = 0; a2 <= i; ++a2) s += __ldg(Tg + a2 + i * HHB) * Zs[a2 * HHU_LC + c];   // T upper triangular
     z2[t] = s;
   }
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < HHB * HHU_BN / HHU_NT; ++t) {
     const int e = tid + t * HHU_NT, i = e % HHB, c = e / HHB;
-    Zs[i][c] = z2[t];
+    Zs[i * HHU_LC + c] = z2[t];
   }
-  // pass 2: C -= V Z2, chunk by chunk
-  for (int r0 = 0; r0 < rows; r0 += HHU_RK) {
+  __syncthreads();
+  // pass 2: C -= V Z2, chunk by chunk (same pipeline), results stored from shared memory
+  for (int s = 0; s < HHU_ST - 1; ++s) issue(s);
+  for (int ch = 0; ch < nch; ++ch) {
+    issue(ch + HHU_ST - 1);
+    cp_async_wait<HHU_ST - 1>();
     __syncthreads();
-    load_chunk(r0);
-    __syncthreads();
+    const double* vs = Vs + (size_t)(ch % HHU_ST) * HHU_RK * HHU_LV;
+    double* cs = Cs + (size_t)(ch % HHU_ST) * HHU_RK * HHU_LC;
     double o[2][2][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -1238,9 +1258,9 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
     for (int kk = 0; kk < HHB; kk += 4) {
       double a[2], b[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) a[i] = Vs[wm + i * 8 + (lane >> 2)][kk + (lane & 3)];
+      for (int i = 0; i < 2; ++i) a[i] = vs[(wm + i * 8 + (lane >> 2)) * HHU_LV + kk + (lane & 3)];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) b[q] = Zs[kk + (lane & 3)][wn + q * 8 + (lane >> 2)];
+      for (int q = 0; q < 2; ++q) b[q] = Zs[(kk + (lane & 3)) * HHU_LC + wn + q * 8 + (lane >> 2)];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -1251,16 +1271,20 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
 #pragma unroll
       for (int q = 0; q < 2; ++q)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) Cs[wm + i * 8 + (lane >> 2)][wn + q * 8 + (lane & 3) * 2 + e] -= o[i][q][e];
+        for (int e = 0; e < 2; ++e) cs[(wm + i * 8 + (lane >> 2)) * HHU_LC + wn + q * 8 + (lane & 3) * 2 + e] -= o[i][q][e];
     __syncthreads();
+    const int r0 = ch * HHU_RK;
     for (int e = tid; e < HHU_RK * HHU_BN; e += HHU_NT) {
       const int rr = e % HHU_RK, c = e / HHU_RK, gr = r0 + rr;
-      if (gr < rows && c < ncb) C[(size_t)c * ld + gr] = Cs[rr][c];
+      if (gr < rows && c < ncb) C[(size_t)c * ld + gr] = cs[rr * HHU_LC + c];
     }
+    __syncthreads();
   }
+  cp_async_wait<0>();
 }
 void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s) {
-  LAUNCH(hh_update_kernel, ntiles, HHU_NT, 0, s, static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j);
+  ensure_dyn_smem(hh_update_kernel, HHU_SMEM);
+  LAUNCH(hh_update_kernel, ntiles, HHU_NT, HHU_SMEM, s, static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j);
 }
 
 // M = R^T (m x r) from the upper triangle of the factored A (n x m, lda)

@@ -177,6 +177,7 @@ class DevPool {
   }
   void recycle() { reset(); }
   size_t total() const { return held_; }
+  size_t nchunks() const { return chunks_.size(); }
 
  private:
   std::vector<std::pair<void*, size_t>> chunks_;
