@@ -15,7 +15,6 @@ workload, timed on the host cores (rank 0 only).
 from __future__ import annotations
 
 import argparse
-import dataclasses
 import json
 import os
 import subprocess
@@ -29,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_2301_12704_b200 import workloads as W  # noqa: E402
+from paper_2301_12704_b200 import dist as D  # noqa: E402
 
 METRIC = "AIFMM factor+solve unknowns/sec"
 UNIT = "unknowns/s"
@@ -166,7 +166,7 @@ def run_ours(args, cfg):
     # N > 1: every rank factors its own independent instance of the workload (same
     # distribution, kernel, leaf size, tol, nrhs; rank-offset seed): weak scaling over
     # independent problems, no data-path collective
-    cfg_r = cfg if rank == 0 else dataclasses.replace(cfg, seed=cfg.seed + 1000 * rank)
+    cfg_r = D.instance_config(cfg, rank)
     pts, b = W.make(cfg_r)
     P = torch.from_numpy(pts).to(dev)
     B = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
@@ -216,11 +216,8 @@ def run_ours(args, cfg):
     clk = clocks.stop()
     step_ms = (tb + tf + ts) / args.steps
     fs_ms = (tf + ts) / args.steps
-    if world > 1:
-        t = torch.tensor([fs_ms, step_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        fs_ms, step_ms = float(t[0]), float(t[1])
-    value = world * cfg.n / (fs_ms / 1e3)
+    fs_ms, step_ms = D.max_over_ranks([fs_ms, step_ms], dev)
+    value = D.aggregate_throughput(cfg.n, world, fs_ms / 1e3)
 
     # end-to-end: host points + host B through the public API, copies inside the region
     pts_h = torch.from_numpy(pts).pin_memory()
@@ -238,7 +235,7 @@ def run_ours(args, cfg):
         Xh = A.solve_host(Bh.copy())
         torch.cuda.synchronize()
         e2e_t.append(time.perf_counter() - t0)
-    e2e_value = world * cfg.n / float(np.mean(e2e_t))
+    e2e_value = D.aggregate_throughput(cfg.n, world, D.max_over_ranks([float(np.mean(e2e_t))], dev)[0])
 
     # correctness guard on the last device result (sampled direct-sum residual)
     res = None

@@ -1109,7 +1109,80 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   if (g_prof.on) g_prof.end("cmp.redirect");
 }
 
-static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
+// Host plan of a colour's Schur updates (Table 4, Alg. 3), built BEFORE
+// the colour's compression so that it overlaps the GPU work still queued for the previous colour.
+// Nothing in it depends on the ranks the compression decides: targets are neighbours of the
+// colour's boxes (live sizes fixed), block pointers do not move (regrow() only touches blocks of
+// boxes that are not eliminated), and the operand W_i = G[:, 0:m] R_i is referenced by column
+// offset and patched once n_i = m_i + k_i is known.
+struct SchurPlan {
+  GemmBatch g;
+  struct Fix { size_t term; int a, off; };
+  std::vector<Fix> fix;
+  std::vector<std::vector<int>> nbs;
+  std::vector<std::vector<std::pair<int, int>>> wcol;   // (q, column offset in W_i)
+  std::vector<int> tot;
+  std::vector<std::pair<int, int>> new_pending;
+};
+static int wcol_of(const std::vector<std::pair<int, int>>& w, int q) {
+  for (auto& e : w)
+    if (e.first == q) return e.second;
+  return -1;
+}
+static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
+  const int l = f.l;
+  g_prof.hstart();
+  P.nbs.assign(cs.size(), {});
+  P.wcol.assign(cs.size(), {});
+  P.tot.assign(cs.size(), 0);
+  for (size_t a = 0; a < cs.size(); ++a) {
+    const int i = cs[a];
+    int nn_;
+    const int* nl = c.nlist(l, i, &nn_);
+    int tot = 0;
+    for (int t = 0; t < nn_; ++t)
+      if (nl[t] != i) { P.nbs[a].push_back(nl[t]); P.wcol[a].push_back({nl[t], tot}); tot += live(f, nl[t]); }
+    P.tot[a] = tot;
+  }
+  // (p, q, a) triples sorted by target then by a (ascending eliminated box = fixed order)
+  struct Tg { long long key; int a; };
+  std::vector<Tg> tgs;
+  for (size_t a = 0; a < cs.size(); ++a)
+    for (int p : P.nbs[a])
+      for (int q : P.nbs[a]) tgs.push_back(Tg{f.key(p, q), (int)a});
+  std::sort(tgs.begin(), tgs.end(), [](const Tg& x, const Tg& y) { return x.key < y.key || (x.key == y.key && x.a < y.a); });
+  g_prof.hlap("tg.sort");
+  std::vector<int> grp_a;
+  for (size_t t0 = 0; t0 < tgs.size();) {
+    size_t t1 = t0;
+    grp_a.clear();
+    while (t1 < tgs.size() && tgs[t1].key == tgs[t0].key) grp_a.push_back(tgs[t1++].a);
+    const int p = (int)(tgs[t0].key / f.nb), q = (int)(tgs[t0].key % f.nb);
+    t0 = t1;
+    const int M = live(f, p), N = live(f, q);
+    if (!M || !N) continue;
+    Blk T;
+    auto it = f.nearb.find(f.key(p, q));
+    if (it != f.nearb.end()) T = it->second;
+    else if (f.E[p] && f.E[q]) T = f.A.at(f.key(p, q));
+    else {
+      T = f.F.at(f.key(p, q));
+      AIFMM_REQUIRE(c.cheb(l, p, q) == 2, AIFMM_ESINGULAR_PIVOT, "fill-in outside N and IL");
+      P.new_pending.push_back({std::min(p, q), std::max(p, q)});
+    }
+    P.g.task(T.p, T.ld, M, N, 1.0);
+    for (int a : grp_a) {
+      const int i = cs[a];
+      if (!f.m[i]) continue;
+      const Blk& C = f.nearb.at(f.key(p, i));
+      P.fix.push_back({P.g.nterms(), a, wcol_of(P.wcol[a], q)});
+      P.g.term(-1.0, C.p, C.ld, 0, nullptr, 0, 0, f.m[i]);   // B patched in eliminate_colour
+    }
+  }
+  g_prof.hlap("tg.tasks");
+}
+
+static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
   const int l = f.l;
   if (g_prof.on) g_prof.begin(c.s);
   // 1. assemble P_i = [[K_ii, U_i],[V_i^T, 0]] into G_i and invert in place (R16)
@@ -1134,74 +1207,39 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
   batched_inverse(inv, c.work, c.up, c.s, &c.fc_all);
   if (g_prof.on) { g_prof.end("elim.inverse"); g_prof.begin(c.s); }
   // 2. W_i = G[:, 0:m] * R_i (row X_i blocks), columns ordered as N(i) \ i
-  std::vector<std::vector<int>> nbs(cs.size());
   std::vector<double*> W(cs.size());
-  std::vector<std::unordered_map<int, int>> wcol(cs.size());
   GemmBatch g;
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];
     const int m = f.m[i], n = m + f.k[i];
-    int nn_;
-    const int* nl = c.nlist(l, i, &nn_);
-    int tot = 0;
-    for (int t = 0; t < nn_; ++t)
-      if (nl[t] != i) { nbs[a].push_back(nl[t]); wcol[a][nl[t]] = tot; tot += live(f, nl[t]); }
-    W[a] = c.work.d(std::max<size_t>((size_t)n * tot, 1));
+    W[a] = c.work.d(std::max<size_t>((size_t)n * P.tot[a], 1));
     if (!n) continue;
-    for (int q : nbs[a]) {
+    for (auto& wq : P.wcol[a]) {
+      const int q = wq.first;
       const Blk& R = f.nearb.at(f.key(i, q));
       if (!live(f, q)) continue;
-      g.task(W[a] + (size_t)wcol[a][q] * n, n, n, live(f, q), 0.0);
+      g.task(W[a] + (size_t)wq.second * n, n, n, live(f, q), 0.0);
       g.term(1.0, f.rec[i].G, n, 0, R.p, R.ld, 0, m);
     }
   }
   g.run(c.up, c.s, &c.fc_all);
   if (g_prof.on) { g_prof.end("elim.W"); g_prof.begin(c.s); }
-  // 3. Schur updates, target-centric (deterministic ascending-i accumulation), + new blocks
-  // (p, q, a) triples sorted by target then by a (ascending eliminated box = fixed order)
+  // 3. Schur updates (planned), then the new blocks (p,i) = C G12, (i,q) = G21 R = W_z,
+  //    (i,i) = -G22 (R17)
   g_prof.hstart();
-  struct Tg { long long key; int a; };
-  std::vector<Tg> tgs;
-  for (size_t a = 0; a < cs.size(); ++a)
-    for (int p : nbs[a])
-      for (int q : nbs[a]) tgs.push_back(Tg{f.key(p, q), (int)a});
-  std::sort(tgs.begin(), tgs.end(), [](const Tg& x, const Tg& y) { return x.key < y.key || (x.key == y.key && x.a < y.a); });
-  g_prof.hlap("tg.sort");
-  std::vector<int> grp_a;
-  for (size_t t0 = 0; t0 < tgs.size();) {
-    size_t t1 = t0;
-    grp_a.clear();
-    while (t1 < tgs.size() && tgs[t1].key == tgs[t0].key) grp_a.push_back(tgs[t1++].a);
-    const int p = (int)(tgs[t0].key / f.nb), q = (int)(tgs[t0].key % f.nb);
-    t0 = t1;
-    const int M = live(f, p), N = live(f, q);
-    if (!M || !N) continue;
-    Blk T;
-    auto it = f.nearb.find(f.key(p, q));
-    if (it != f.nearb.end()) T = it->second;
-    else if (f.E[p] && f.E[q]) T = f.A.at(f.key(p, q));
-    else {
-      T = f.F.at(f.key(p, q));
-      AIFMM_REQUIRE(c.cheb(l, p, q) == 2, AIFMM_ESINGULAR_PIVOT, "fill-in outside N and IL");
-      f.pending.insert({std::min(p, q), std::max(p, q)});
-    }
-    g.task(T.p, T.ld, M, N, 1.0);
-    for (int a : grp_a) {
-      int i = cs[a];
-      const int m = f.m[i], n = m + f.k[i];
-      if (!m) continue;
-      const Blk& C = f.nearb.at(f.key(p, i));
-      g.term(-1.0, C.p, C.ld, 0, W[a] + (size_t)wcol[a][q] * n, n, 0, m);
-    }
+  for (const auto& fx : P.fix) {
+    const int n = f.m[cs[fx.a]] + f.k[cs[fx.a]];
+    GemmTerm& t = P.g.term_ref(fx.term);
+    t.B = W[fx.a] + (size_t)fx.off * n;
+    t.ldb = n;
   }
-  g_prof.hlap("tg.tasks");
-  // new blocks (p,i) = C G12, (i,q) = G21 R = W_z, (i,i) = -G22 (R17)
+  for (auto& pr : P.new_pending) f.pending.insert(pr);
   std::vector<std::pair<long long, Blk>> fresh;
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];
     const int m = f.m[i], k = f.k[i], n = m + k;
     Rec& r = f.rec[i];
-    for (int p : nbs[a]) {
+    for (int p : P.nbs[a]) {
       const Blk& C = f.nearb.at(f.key(p, i));
       r.C.push_back({p, C});
       r.Ckind_z.push_back(f.E[p]);
@@ -1209,18 +1247,19 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
       DevPool& bp = f.E[p] ? c.scr(l) : c.persist;
       Blk nb_{bp.d(std::max<size_t>((size_t)live(f, p) * k, 1)), std::max(live(f, p), 1), live(f, p), k};
       if (live(f, p) && k) {
-        g.task(nb_.p, nb_.ld, live(f, p), k, 0.0);
-        if (m) g.term(1.0, C.p, C.ld, 0, r.G + (size_t)m * n, n, 0, m);
+        P.g.task(nb_.p, nb_.ld, live(f, p), k, 0.0);
+        if (m) P.g.term(1.0, C.p, C.ld, 0, r.G + (size_t)m * n, n, 0, m);
       }
       fresh.push_back({f.key(p, i), nb_});
     }
-    for (int q : nbs[a]) {
+    for (auto& wq : P.wcol[a]) {
+      const int q = wq.first;
       const Blk& R = f.nearb.at(f.key(i, q));
       r.R.push_back({q, R});
       r.Rkind_y.push_back(f.E[q]);
       DevPool& bp = f.E[q] ? c.scr(l) : c.persist;
       Blk nb_{bp.d(std::max<size_t>((size_t)k * live(f, q), 1)), std::max(k, 1), k, live(f, q)};
-      cb.copy(W[a] + (size_t)wcol[a][q] * n + m, n, nb_.p, nb_.ld, k, live(f, q));
+      cb.copy(W[a] + (size_t)wq.second * n + m, n, nb_.p, nb_.ld, k, live(f, q));
       fresh.push_back({f.key(i, q), nb_});
     }
     Blk nb_{c.scr(l).d(std::max<size_t>((size_t)k * k, 1)), std::max(k, 1), k, k};
@@ -1236,7 +1275,7 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs) {
   }
   if (g_prof.on) { g_prof.end("elim.plan"); g_prof.begin(c.s); }
   long long l0 = g_launches;
-  g.run(c.up, c.s, &c.fc_schur);
+  P.g.run(c.up, c.s, &c.fc_schur);
   c.stats[AIFMM_STAT_SCHUR_LAUNCHES] += (double)(g_launches - l0);
   if (c.timing) {
     AIFMM_CUDA(cudaEventRecord(e1, c.s));
@@ -1271,11 +1310,13 @@ static void factor_all(Ctx& c) {
       std::vector<std::pair<int, int>> S;
       for (auto& pr : f.pending)
         if (c.col[l][pr.first] == col || c.col[l][pr.second] == col) S.push_back(pr);
+      SchurPlan plan;
+      plan_schur(c, f, cs, plan);   // host work, overlaps the previous colour's kernels
       g_prof.begin(c.s);
       if (!S.empty()) compress(c, f, S);
       g_prof.end(("compress.L" + std::to_string(l)).c_str());
       g_prof.begin(c.s);
-      eliminate_colour(c, f, cs);
+      eliminate_colour(c, f, cs, plan);
       g_prof.end(("eliminate.L" + std::to_string(l)).c_str());
     }
     AIFMM_REQUIRE(f.pending.empty(), AIFMM_ESINGULAR_PIVOT, "pending far fill-ins at level end");

@@ -38,18 +38,24 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // Batched variable-size GEMM on FP64 tensor cores.  One CTA = one BM x BN tile of one task;
 // the K loop runs over all terms of the task (deterministic order), operand tiles are staged
-// global -> shared by cp.async with a 2-stage double buffer, each warp owns a 32 x 32 sub-tile
-// (4 x 4 DMMA 8x8x4 fragments), alpha is applied to the A fragments in registers.
+// global -> shared by cp.async through a GEMM_ST-stage ring (dynamic shared memory), each warp
+// owns a 32 x 32 sub-tile (4 x 4 DMMA 8x8x4 fragments), alpha is applied to the A fragments.
+constexpr int GEMM_ST = 2, GEMM_BK = 16;   // measured: 2 stages beat 3 and 4 (occupancy: 118 registers)
+template <int BM, int BN>
+constexpr size_t gemm_smem() { return sizeof(double) * (size_t)GEMM_ST * GEMM_BK * ((BM + 4) + (BN + 4)); }
+
 template <int BM, int BN>
 __global__ void __launch_bounds__(BM * BN / 32)
 gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmTerm* __restrict__ terms,
                   const GemmTile* __restrict__ tiles) {
-  constexpr int BK = 16;
+  constexpr int BK = GEMM_BK, ST = GEMM_ST;
   constexpr int NT = BM * BN / 32;
   constexpr int LDS_A = BM + 4;              // (BM+4) % 16 == 4 -> conflict-free fragment loads
   constexpr int LDS_B = BN + 4;
-  __shared__ __align__(16) double sA[2][BK][LDS_A];
-  __shared__ __align__(16) double sB[2][BK][LDS_B];
+  extern __shared__ __align__(16) double gsm[];
+  double* sA = gsm;                          // [ST][BK][LDS_A]
+  double* sB = gsm + (size_t)ST * BK * LDS_A; // [ST][BK][LDS_B]
+  __shared__ double s_alpha[ST];
 
   const GemmTile tile = tiles[blockIdx.x];
   const GemmTask tk = tasks[tile.task];
@@ -64,67 +70,68 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmTerm* __restrict
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // iteration state over (term, k0) K-tiles of the multiplicative terms
   auto next_term = [&](int t) {
     while (t < tk.term_end && terms[t].A == nullptr) ++t;
     return t;
   };
-  auto load = [&](int st, int t, int k0) {
+  int nk = 0;                                // number of (term, k0) tiles of this task
+  for (int t = tk.term_begin; t < tk.term_end; ++t) {
     const GemmTerm tm = terms[t];
-    for (int e = tid; e < BM * BK; e += NT) {
-      int mm, kk;
-      if (!tm.transA) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
-      const int gm = m0 + mm, gk = k0 + kk;
-      const bool ok = gm < tk.M && gk < tm.K;
-      const double* src = ok ? (tm.transA ? tm.A + (size_t)gm * tm.lda + gk : tm.A + (size_t)gk * tm.lda + gm) : tm.A;
-      cp_async8(&sA[st][kk][mm], src, ok);
-    }
-    for (int e = tid; e < BN * BK; e += NT) {
-      int nn, kk;
-      if (!tm.transB) { kk = e % BK; nn = e / BK; } else { nn = e % BN; kk = e / BN; }
-      const int gn = n0 + nn, gk = k0 + kk;
-      const bool ok = gn < tk.N && gk < tm.K;
-      const double* src = ok ? (tm.transB ? tm.B + (size_t)gk * tm.ldb + gn : tm.B + (size_t)gn * tm.ldb + gk) : tm.B;
-      cp_async8(&sB[st][kk][nn], src, ok);
-    }
-  };
-  int ct = next_term(tk.term_begin), ck = 0;
-  if (ct < tk.term_end) {
-    load(0, ct, 0);
-    cp_async_commit();
+    if (tm.A) nk += (tm.K + BK - 1) / BK;
   }
-  int st = 0;
-  while (ct < tk.term_end) {
-    // lookahead position
-    int nt = ct, nk = ck + BK;
-    if (nk >= terms[ct].K) { nt = next_term(ct + 1); nk = 0; }
-    const bool more = nt < tk.term_end;
-    if (more) {
-      load(st ^ 1, nt, nk);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+  int lt = next_term(tk.term_begin), lk = 0; // next tile to load
+  auto load_next = [&](int st) {
+    if (lt < tk.term_end) {
+      const GemmTerm tm = terms[lt];
+      double* a_s = sA + (size_t)st * BK * LDS_A;
+      double* b_s = sB + (size_t)st * BK * LDS_B;
+      for (int e = tid; e < BM * BK; e += NT) {
+        int mm, kk;
+        if (!tm.transA) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
+        const int gm = m0 + mm, gk = lk + kk;
+        const bool ok = gm < tk.M && gk < tm.K;
+        const double* src = ok ? (tm.transA ? tm.A + (size_t)gm * tm.lda + gk : tm.A + (size_t)gk * tm.lda + gm) : tm.A;
+        cp_async8(a_s + kk * LDS_A + mm, src, ok);
+      }
+      for (int e = tid; e < BN * BK; e += NT) {
+        int nn, kk;
+        if (!tm.transB) { kk = e % BK; nn = e / BK; } else { nn = e % BN; kk = e / BN; }
+        const int gn = n0 + nn, gk = lk + kk;
+        const bool ok = gn < tk.N && gk < tm.K;
+        const double* src = ok ? (tm.transB ? tm.B + (size_t)gk * tm.ldb + gn : tm.B + (size_t)gn * tm.ldb + gk) : tm.B;
+        cp_async8(b_s + kk * LDS_B + nn, src, ok);
+      }
+      if (tid == 0) s_alpha[st] = tm.alpha;
+      lk += BK;
+      if (lk >= tm.K) { lt = next_term(lt + 1); lk = 0; }
     }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) load_next(s);
+  for (int it = 0; it < nk; ++it) {
+    load_next((it + ST - 1) % ST);
+    cp_async_wait<ST - 1>();
     __syncthreads();
-    const double alpha = terms[ct].alpha;
+    const int st = it % ST;
+    const double alpha = s_alpha[st];
+    const double* a_s = sA + (size_t)st * BK * LDS_A;
+    const double* b_s = sB + (size_t)st * BK * LDS_B;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double a[4], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = alpha * sA[st][kk + (lane & 3)][wm + i * 8 + (lane >> 2)];
+      for (int i = 0; i < 4; ++i) a[i] = alpha * a_s[(kk + (lane & 3)) * LDS_A + wm + i * 8 + (lane >> 2)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = sB[st][kk + (lane & 3)][wn + j * 8 + (lane >> 2)];
+      for (int j = 0; j < 4; ++j) b[j] = b_s[(kk + (lane & 3)) * LDS_B + wn + j * 8 + (lane >> 2)];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
     __syncthreads();
-    st ^= 1;
-    ct = nt;
-    ck = nk;
   }
+  cp_async_wait<0>();
   // epilogue: C = beta*C + acc + sum(addition terms)
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -207,6 +214,26 @@ __device__ __forceinline__ int block_min_int(int v, int* red) {
   int r = red[0];
   __syncthreads();
   return r;
+}
+
+// (max |x|, lowest index attaining it) over the block in one shared-memory round
+template <int NT>
+__device__ __forceinline__ void block_argmax(double v, int idx, double* redv, int* redi, double* mx, int* at) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) { redv[w] = v; redi[w] = idx; }
+  __syncthreads();
+  double bv = redv[0];
+  int bi = redi[0];
+  for (int q = 1; q < NT / 32; ++q)
+    if (redv[q] > bv || (redv[q] == bv && redi[q] < bi)) { bv = redv[q]; bi = redi[q]; }
+  *mx = bv;
+  *at = bi;
 }
 
 // ------------------------------------------------------------------------------ Gauss-Jordan
@@ -333,19 +360,20 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
   __shared__ double Li[GJB][GJB + 1], Ui[GJB][GJB + 1], Di[GJB][GJB + 1];
   __shared__ double ycol[GJ_NT / 32][GJB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int e = tid; e < rows * nbw; e += GJ_NT) {
-    const int r = e % rows, c = e / rows;
-    PW[(size_t)c * rows + r] = A[(size_t)(j + c) * ld + j + r];
-  }
+  for (int c = warp; c < nbw; c += GJ_NT / 32)
+    for (int r = lane; r < rows; r += 32) PW[(size_t)c * rows + r] = A[(size_t)(j + c) * ld + j + r];
   __syncthreads();
   for (int c = 0; c < nbw; ++c) {
+    // pivot: largest |entry|, lowest row among equal ones (same rule as before, one reduction)
     double v = -1.0;
-    for (int r = c + tid; r < rows; r += GJ_NT) v = fmax(v, fabs(PW[(size_t)c * rows + r]));
-    const double mx = block_max<GJ_NT>(v, red);
-    int cand = 0x7fffffff;
-    for (int r = c + tid; r < rows; r += GJ_NT)
-      if (fabs(PW[(size_t)c * rows + r]) == mx) { cand = r; break; }
-    const int p = block_min_int<GJ_NT>(cand, redi);
+    int vi = 0x7fffffff;
+    for (int r = c + tid; r < rows; r += GJ_NT) {
+      const double a = fabs(PW[(size_t)c * rows + r]);
+      if (a > v) { v = a; vi = r; }
+    }
+    double mx;
+    int p;
+    block_argmax<GJ_NT>(v, vi, red, redi, &mx, &p);
     if (!(mx > 0.0)) {
       if (tid == 0) *tk.info = j + c + 1;
       return;
@@ -361,24 +389,33 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
     const double dinv = 1.0 / PW[(size_t)c * rows + c];
     for (int r = c + 1 + tid; r < rows; r += GJ_NT) PW[(size_t)c * rows + r] *= dinv;
     __syncthreads();
-    const int rem = rows - c - 1, cw = nbw - c - 1;
-    for (int e = tid; e < rem * cw; e += GJ_NT) {
-      const int r = c + 1 + e % rem, cc = c + 1 + e / rem;
-      PW[(size_t)cc * rows + r] -= PW[(size_t)c * rows + r] * PW[(size_t)cc * rows + c];
+    // rank-1 update of the panel: one warp per column, rows coalesced
+    for (int cc = c + 1 + warp; cc < nbw; cc += GJ_NT / 32) {
+      double* y = PW + (size_t)cc * rows;
+      const double f = y[c];
+      const double* x = PW + (size_t)c * rows;
+      for (int r = c + 1 + lane; r < rows; r += 32) y[r] -= x[r] * f;
     }
     __syncthreads();
   }
-  // apply the row interchanges to the full rows of A (in order)
-  for (int c = 0; c < nbw; ++c) {
-    const int p = tk.piv[j + c];
-    if (p != j + c)
-      for (int col = tid; col < n; col += GJ_NT) {
-        double a = A[(size_t)col * ld + j + c], b = A[(size_t)col * ld + p];
-        A[(size_t)col * ld + j + c] = b;
-        A[(size_t)col * ld + p] = a;
+  // apply the row interchanges to the full rows of A (in order): each thread owns whole
+  // columns and applies the panel's swaps in sequence (no barrier per interchange)
+  __syncthreads();
+  __shared__ int pv[GJB];
+  if (tid < nbw) pv[tid] = tk.piv[j + tid];
+  __syncthreads();
+  for (int col = tid; col < n; col += GJ_NT) {
+    double* ac = A + (size_t)col * ld;
+    for (int c = 0; c < nbw; ++c) {
+      const int p = pv[c];
+      if (p != j + c) {
+        const double a = ac[j + c];
+        ac[j + c] = ac[p];
+        ac[p] = a;
       }
-    __syncthreads();
+    }
   }
+  __syncthreads();
   // D^{-1} = U11^{-1} L11^{-1} from the panel LU (unit lower L11, upper U11)
   for (int e = tid; e < GJB * GJB; e += GJ_NT) {
     const int r = e % GJB, c = e / GJB;
@@ -414,12 +451,12 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
   }
   __syncthreads();
   // B = A[:, J] with rows J zeroed, A[R, J] = 0, A[J, J] = D^{-1}
-  for (int e = tid; e < n * nbw; e += GJ_NT) {
-    const int r = e % n, c = e / n;
-    const bool inJ = (r >= j && r < j + nbw);
-    tk.Bws[(size_t)c * n + r] = inJ ? 0.0 : A[(size_t)(j + c) * ld + r];
-    A[(size_t)(j + c) * ld + r] = inJ ? Di[r - j][c] : 0.0;
-  }
+  for (int c = warp; c < nbw; c += GJ_NT / 32)
+    for (int r = lane; r < n; r += 32) {
+      const bool inJ = (r >= j && r < j + nbw);
+      tk.Bws[(size_t)c * n + r] = inJ ? 0.0 : A[(size_t)(j + c) * ld + r];
+      A[(size_t)(j + c) * ld + r] = inJ ? Di[r - j][c] : 0.0;
+    }
   // A[J, c] <- D^{-1} A[J, c] for columns outside J
   for (int col = warp; col < n; col += GJ_NT / 32) {
     if (col >= j && col < j + nbw) continue;
@@ -434,18 +471,191 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
   }
 }
 
+// Cluster variant of the Gauss-Jordan panel for few large matrices (the top system, upper-level
+// pivots): the GJC CTAs of a cluster own contiguous row slices of the panel in shared memory.
+// Per column one cluster barrier: every CTA publishes its local pivot candidate (value, row and
+// the whole candidate row) and, if it owns row c, row c; afterwards every CTA knows the pivot row
+// and the owner of the pivot row swaps in the old row c.  Same pivot rule as gj_panel_kernel
+// (largest |entry|, lowest row on ties).  The interchanges of the full rows, D^{-1} and the
+// B / A[J, :] writes are split over the cluster as well.
+constexpr int GJC = 8;
+struct GjcShared {
+  double v[2];
+  int idx[2];
+  double cand[2][GJB];   // the candidate row of this CTA
+  double rowc[2][GJB];   // row c, if this CTA owns it
+  double D[GJB][GJB + 1];
+};
+__global__ void __cluster_dims__(GJC, 1, 1) __launch_bounds__(GJ_NT)
+gj_panel_cluster_kernel(const GJBTask* __restrict__ tasks, int j, int cap_rows) {
+  extern __shared__ double gjc_p[];      // own panel rows: cnt x GJB, row-major (ld GJB + 1)
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const GJBTask tk = tasks[blockIdx.x / GJC];
+  const int n = tk.n;
+  if (j >= n) return;                    // uniform over the cluster
+  if (*tk.info) return;
+  const int nbw = min(GJB, n - j), rows = n - j, ld = tk.lda;
+  const int chunk = (rows + GJC - 1) / GJC;
+  const int lo = min(rows, rank * chunk), hi = min(rows, lo + chunk), cnt = hi - lo;
+  constexpr int LP = GJB + 1;
+  double* P = gjc_p;
+  __shared__ GjcShared sh;
+  __shared__ double red[32];
+  __shared__ int redi[32];
+  __shared__ double prow[GJB];
+  __shared__ double Li[GJB][GJB + 1], Ui[GJB][GJB + 1];
+  __shared__ int pv[GJB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* A = tk.A;
+  for (int c = warp; c < nbw; c += GJ_NT / 32)
+    for (int r = lane; r < cnt; r += 32) P[r * LP + c] = A[(size_t)(j + c) * ld + j + lo + r];
+  __syncthreads();
+  int ph = 0;
+  for (int c = 0; c < nbw; ++c) {
+    // local candidate: largest |P[r][c]| over own rows r >= c, lowest row on ties
+    double v = -1.0;
+    int vi = 0x7fffffff;
+    for (int r = max(c - lo, 0) + tid; r < cnt; r += GJ_NT) {
+      const double a = fabs(P[r * LP + c]);
+      if (a > v) { v = a; vi = lo + r; }
+    }
+    double mx;
+    int p;
+    block_argmax<GJ_NT>(v, vi, red, redi, &mx, &p);
+    if (tid == 0) { sh.v[ph] = mx; sh.idx[ph] = p; }
+    if (p >= lo && p < hi)
+      for (int cc = tid; cc < nbw; cc += GJ_NT) sh.cand[ph][cc] = P[(p - lo) * LP + cc];
+    if (c >= lo && c < hi)
+      for (int cc = tid; cc < nbw; cc += GJ_NT) sh.rowc[ph][cc] = P[(c - lo) * LP + cc];
+    cl.sync();
+    // global pivot
+    double gm = -1.0;
+    int gp = 0x7fffffff, go = 0;
+    for (int q = 0; q < GJC; ++q) {
+      const GjcShared* o = cl.map_shared_rank(&sh, q);
+      const double ov = o->v[ph];
+      const int oi = o->idx[ph];
+      if (ov > gm || (ov == gm && oi < gp)) { gm = ov; gp = oi; go = q; }
+    }
+    if (!(gm > 0.0)) {
+      if (rank == 0 && tid == 0) *tk.info = j + c + 1;
+      cl.sync();
+      return;
+    }
+    const int oc = min(GJC - 1, c / chunk);   // owner of row c
+    if (rank == 0 && tid == 0) tk.piv[j + c] = j + gp;
+    // pivot row (old row gp) for everyone; the owner of gp receives old row c
+    const GjcShared* wo = cl.map_shared_rank(&sh, go);
+    for (int cc = tid; cc < nbw; cc += GJ_NT) prow[cc] = wo->cand[ph][cc];
+    if (gp != c && gp >= lo && gp < hi) {
+      const GjcShared* co = cl.map_shared_rank(&sh, oc);
+      for (int cc = tid; cc < nbw; cc += GJ_NT) P[(gp - lo) * LP + cc] = co->rowc[ph][cc];
+    }
+    __syncthreads();
+    if (c >= lo && c < hi)
+      for (int cc = tid; cc < nbw; cc += GJ_NT) P[(c - lo) * LP + cc] = prow[cc];
+    // scale the column below the diagonal and update the trailing panel columns (own rows)
+    const double dinv = 1.0 / prow[c];
+    for (int r = max(c + 1 - lo, 0) + tid; r < cnt; r += GJ_NT) {
+      double* pr = P + r * LP;
+      const double l = pr[c] * dinv;
+      pr[c] = l;
+      for (int cc = c + 1; cc < nbw; ++cc) pr[cc] -= l * prow[cc];
+    }
+    __syncthreads();
+    ph ^= 1;
+  }
+  // panel LU back to PW (rows relative to j, ld rows) for D
+  for (int c = warp; c < nbw; c += GJ_NT / 32)
+    for (int r = lane; r < cnt; r += 32) tk.PW[(size_t)c * rows + lo + r] = P[r * LP + c];
+  cl.sync();
+  if (tid < nbw) pv[tid] = tk.piv[j + tid];
+  // interchanges of the full rows: columns split over the cluster
+  const int cw = (n + GJC - 1) / GJC, c0 = min(n, rank * cw), c1 = min(n, c0 + cw);
+  __syncthreads();
+  for (int col = c0 + tid; col < c1; col += GJ_NT) {
+    double* ac = A + (size_t)col * ld;
+    for (int c = 0; c < nbw; ++c) {
+      const int p = pv[c];
+      if (p != j + c) {
+        const double a = ac[j + c];
+        ac[j + c] = ac[p];
+        ac[p] = a;
+      }
+    }
+  }
+  // D^{-1} = U11^{-1} L11^{-1} (rank 0), shared through DSMEM
+  const double* PW = tk.PW;
+  if (rank == 0) {
+    for (int e = tid; e < GJB * GJB; e += GJ_NT) { Li[e % GJB][e / GJB] = 0.0; Ui[e % GJB][e / GJB] = 0.0; }
+    __syncthreads();
+    if (warp == 0) {
+      if (lane < nbw)
+        for (int r = 0; r < nbw; ++r) {
+          double s = (r == lane) ? 1.0 : 0.0;
+          for (int t = lane; t < r; ++t) s -= PW[(size_t)t * rows + r] * Li[t][lane];
+          Li[r][lane] = (r < lane) ? 0.0 : s;
+        }
+    } else if (warp == 1) {
+      if (lane < nbw)
+        for (int r = nbw - 1; r >= 0; --r) {
+          double s = (r == lane) ? 1.0 : 0.0;
+          for (int t = r + 1; t <= lane; ++t) s -= PW[(size_t)t * rows + r] * Ui[t][lane];
+          Ui[r][lane] = (r > lane) ? 0.0 : s / PW[(size_t)r * rows + r];
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < nbw * nbw; e += GJ_NT) {
+      const int r = e % nbw, c = e / nbw;
+      double s = 0.0;
+      for (int t = 0; t < nbw; ++t) s += Ui[r][t] * Li[t][c];
+      sh.D[r][c] = s;
+    }
+  }
+  cl.sync();   // row interchanges done everywhere, D published
+  const GjcShared* d0 = cl.map_shared_rank(&sh, 0);
+  for (int e = tid; e < nbw * nbw; e += GJ_NT) Li[e % nbw][e / nbw] = d0->D[e % nbw][e / nbw];   // Li := D
+  __syncthreads();
+  // B = A[:, J] with rows J zeroed, A[R, J] = 0, A[J, J] = D^{-1}: rows split over the cluster
+  const int rw2 = (n + GJC - 1) / GJC, r0 = min(n, rank * rw2), r1 = min(n, r0 + rw2);
+  for (int c = warp; c < nbw; c += GJ_NT / 32)
+    for (int r = r0 + lane; r < r1; r += 32) {
+      const bool inJ = (r >= j && r < j + nbw);
+      tk.Bws[(size_t)c * n + r] = inJ ? 0.0 : A[(size_t)(j + c) * ld + r];
+      A[(size_t)(j + c) * ld + r] = inJ ? Li[r - j][c] : 0.0;
+    }
+  // A[J, col] <- D^{-1} A[J, col] for columns outside J: columns split over the cluster
+  __shared__ double ycol[GJ_NT / 32][GJB];
+  for (int col = c0 + warp; col < c1; col += GJ_NT / 32) {
+    if (col >= j && col < j + nbw) continue;
+    if (lane < nbw) ycol[warp][lane] = A[(size_t)col * ld + j + lane];
+    __syncwarp();
+    if (lane < nbw) {
+      double s = 0.0;
+      for (int t = 0; t < nbw; ++t) s += Li[lane][t] * ycol[warp][t];
+      A[(size_t)col * ld + j + lane] = s;
+    }
+    __syncwarp();
+  }
+  cl.sync();   // keep the cluster's shared memory alive until every CTA has read rank 0's D
+}
+
+// column interchanges in reverse pivot order; each thread owns one row (accesses over the
+// threads of a warp are consecutive rows: coalesced), blockIdx.y splits the rows
 __global__ void gj_unscramble_kernel(const GJBTask* __restrict__ tasks) {
   const GJBTask tk = tasks[blockIdx.x];
   if (*tk.info) return;
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= tk.n) return;
+  double* A = tk.A;
   for (int k = tk.n - 1; k >= 0; --k) {
     const int p = tk.piv[k];
-    if (p != k)
-      for (int i = threadIdx.x; i < tk.n; i += blockDim.x) {
-        double a = tk.A[(size_t)k * tk.lda + i], b = tk.A[(size_t)p * tk.lda + i];
-        tk.A[(size_t)k * tk.lda + i] = b;
-        tk.A[(size_t)p * tk.lda + i] = a;
-      }
-    __syncthreads();
+    if (p != k) {
+      const double a = A[(size_t)k * tk.lda + i];
+      A[(size_t)k * tk.lda + i] = A[(size_t)p * tk.lda + i];
+      A[(size_t)p * tk.lda + i] = a;
+    }
   }
 }
 
@@ -1331,10 +1541,10 @@ __global__ void norm_tasks_kernel(const NormTask* __restrict__ tasks) {
   const NormTask tk = tasks[blockIdx.x];
   __shared__ double red[32];
   double s = 0.0;
-  const int tot = tk.rows * tk.cols;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const double x = tk.A[(size_t)(e / tk.rows) * tk.lda + (e % tk.rows)];
-    s += x * x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = warp; c < tk.cols; c += 8) {          // warp per column, rows coalesced
+    const double* col = tk.A + (size_t)c * tk.lda;
+    for (int r = lane; r < tk.rows; r += 32) s += col[r] * col[r];
   }
   s = block_sum<256>(s, red);
   if (threadIdx.x == 0) *tk.out = sqrt(s);
@@ -1343,11 +1553,19 @@ __global__ void norm_tasks_kernel(const NormTask* __restrict__ tasks) {
 // ------------------------------------------------------------------------------ host launchers
 void launch_gemm(int tileclass, const GemmTask* t, const GemmTerm* tm, const GemmTile* tiles, int ntiles,
                  cudaStream_t s) {
+  static bool init = false;
+  if (!init) {
+    ensure_dyn_smem(gemm_tasks_kernel<32, 32>, gemm_smem<32, 32>());
+    ensure_dyn_smem(gemm_tasks_kernel<64, 32>, gemm_smem<64, 32>());
+    ensure_dyn_smem(gemm_tasks_kernel<32, 64>, gemm_smem<32, 64>());
+    ensure_dyn_smem(gemm_tasks_kernel<64, 64>, gemm_smem<64, 64>());
+    init = true;
+  }
   switch (tileclass) {
-    case 0: LAUNCH((gemm_tasks_kernel<32, 32>), ntiles, 32, 0, s, t, tm, tiles); break;
-    case 1: LAUNCH((gemm_tasks_kernel<64, 32>), ntiles, 64, 0, s, t, tm, tiles); break;
-    case 2: LAUNCH((gemm_tasks_kernel<32, 64>), ntiles, 64, 0, s, t, tm, tiles); break;
-    default: LAUNCH((gemm_tasks_kernel<64, 64>), ntiles, 128, 0, s, t, tm, tiles); break;
+    case 0: LAUNCH((gemm_tasks_kernel<32, 32>), ntiles, 32, (gemm_smem<32, 32>()), s, t, tm, tiles); break;
+    case 1: LAUNCH((gemm_tasks_kernel<64, 32>), ntiles, 64, (gemm_smem<64, 32>()), s, t, tm, tiles); break;
+    case 2: LAUNCH((gemm_tasks_kernel<32, 64>), ntiles, 64, (gemm_smem<32, 64>()), s, t, tm, tiles); break;
+    default: LAUNCH((gemm_tasks_kernel<64, 64>), ntiles, 128, (gemm_smem<64, 64>()), s, t, tm, tiles); break;
   }
 }
 
@@ -1364,13 +1582,23 @@ void launch_gj(const GJTask* t, int ntasks, int nmax, int mode, cudaStream_t s) 
   }
 }
 
+void launch_gj_panel_cluster(const void* t, int ntasks, int j, int nmax, cudaStream_t s) {
+  const int cap = (std::max(nmax - j, 1) + GJC - 1) / GJC;
+  const size_t smem = (size_t)cap * (GJB + 1) * sizeof(double);
+  ensure_dyn_smem(gj_panel_cluster_kernel, smem);
+  LAUNCH(gj_panel_cluster_kernel, ntasks * GJC, GJ_NT, smem, s, static_cast<const GJBTask*>(t), j, cap);
+}
 void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s) {
   const int elems = (160 * 1024) / 8;
   ensure_dyn_smem(gj_panel_kernel, (size_t)elems * 8);
   LAUNCH(gj_panel_kernel, ntasks, GJ_NT, (size_t)elems * 8, s, static_cast<const GJBTask*>(t), j, elems);
 }
-void launch_gj_unscramble(const void* t, int ntasks, cudaStream_t s) {
-  LAUNCH(gj_unscramble_kernel, ntasks, 256, 0, s, static_cast<const GJBTask*>(t));
+void launch_gj_unscramble(const void* t, int ntasks, int nmax, cudaStream_t s) {
+  if (ntasks <= 0) return;
+  dim3 grid(ntasks, (nmax + 127) / 128);
+  gj_unscramble_kernel<<<grid, 128, 0, s>>>(static_cast<const GJBTask*>(t));
+  AIFMM_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 size_t gjb_task_size() { return sizeof(GJBTask); }
 void gjb_make(void* out, double* A, int lda, int n, double* PW, double* Bws, int* piv, int* info) {

@@ -25,7 +25,8 @@ void launch_copy(const CopyTask* t, int ntasks, int ysplit, cudaStream_t s);
 void launch_norm(const NormTask* t, int ntasks, cudaStream_t s);
 void launch_chol_inv(const CholTask* t, int ntasks, int kmax, cudaStream_t s);
 void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s);
-void launch_gj_unscramble(const void* t, int ntasks, cudaStream_t s);
+void launch_gj_panel_cluster(const void* t, int ntasks, int j, int nmax, cudaStream_t s);
+void launch_gj_unscramble(const void* t, int ntasks, int nmax, cudaStream_t s);
 size_t gjb_task_size();
 void gjb_make(void* out, double* A, int lda, int n, double* PW, double* Bws, int* piv, int* info);
 size_t hh_task_size();
@@ -36,6 +37,17 @@ void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, c
 constexpr int HH_PANEL = 32;
 constexpr int GJ_SMALL_MAX = 160;  // in-place inverses up to this size run in shared memory (<= 206 KB)
 constexpr int GJ_PANEL = 32;
+
+// Batches with >= 296 independent tasks, or >= this many moderate-size ones, run one CTA per
+// task (they fill the GPU); smaller batches of long tasks spread each task over an 8-CTA
+// cluster (measured on configs 2 and 3).  AIFMM_MANY overrides.
+inline int many_threshold() {
+  static const int v = [] {
+    const char* e = getenv("AIFMM_MANY");
+    return e ? atoi(e) : 96;
+  }();
+  return v;
+}
 
 // Optional phase profile (AIFMM_PROFILE=1): synchronises at phase boundaries and prints a
 // breakdown to stderr at the end of factor / solve.  Off by default (no extra syncs).
@@ -272,6 +284,8 @@ class GemmBatch {
   void add(double alpha, const double* B, int ldb, int transB) { term(alpha, nullptr, 0, 0, B, ldb, transB, 0); }
   bool empty() const { return tasks_.empty(); }
   size_t size() const { return tasks_.size(); }
+  size_t nterms() const { return terms_.size(); }
+  GemmTerm& term_ref(size_t i) { return terms_[i]; }
   // Deterministic split-K: single-term tasks with a long K and few output tiles are split into
   // S partial GEMMs into workspace slices, then reduced in a fixed order by a second launch.
   void set_splitk_pool(DevPool* p) { splitk_ = p; }
@@ -430,8 +444,12 @@ inline void batched_inverse(const std::vector<InvReq>& reqs, Pool& work, Uploade
     nmax = std::max(nmax, r.n);
   }
   const void* dt = up.put(tb.data(), tb.size());
+  // few matrices: 8-CTA clusters per matrix (row slices in shared memory); many: one CTA each
+  static const bool gj_single = getenv("AIFMM_GJ_SINGLE") != nullptr;   // debug toggle
+  const bool cluster = !gj_single && (int)big.size() * 4 < 148 * 2 && nmax <= 8 * 700;
   for (int j = 0; j < nmax; j += GJ_PANEL) {
-    launch_gj_panel(dt, (int)big.size(), j, s);
+    if (cluster) launch_gj_panel_cluster(dt, (int)big.size(), j, nmax, s);
+    else launch_gj_panel(dt, (int)big.size(), j, s);
     GemmBatch g;
     for (size_t i = 0; i < big.size(); ++i) {
       const InvReq& r = big[i];
@@ -448,7 +466,7 @@ inline void batched_inverse(const std::vector<InvReq>& reqs, Pool& work, Uploade
     }
     g.run(up, s);
   }
-  launch_gj_unscramble(dt, (int)big.size(), s);
+  launch_gj_unscramble(dt, (int)big.size(), nmax, s);
 }
 
 
@@ -473,7 +491,10 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
   // enough tasks to fill the GPU with one CTA each: no clusters (their 8x more CTAs only add
   // waves of latency-bound panel steps)
   static const bool hh_cluster = getenv("AIFMM_HH_CLUSTER") != nullptr;   // debug toggle
-  const bool many = !hh_cluster && reqs.size() >= 2 * 148;
+  int nmax_rows = 0;
+  for (const auto& q : reqs) nmax_rows = std::max(nmax_rows, q.n);
+  const bool many = !hh_cluster && ((int)reqs.size() >= 2 * 148 ||
+                                    ((int)reqs.size() >= many_threshold() && nmax_rows <= 4096));
   for (const auto& q : reqs) if (q.n < 512 || many) sorted_reqs.push_back(q);
   const size_t nsmall = sorted_reqs.size();
   int nmax_mid = 0;
@@ -529,7 +550,9 @@ inline void run_pqr(const std::vector<PqrTask>& v, Uploader& up, cudaStream_t s)
   std::vector<PqrTask> small, big;
   size_t smem = 0;
   // many tasks: one CTA each fills the GPU; few tall tasks: 8-CTA clusters
-  const bool many = v.size() >= 2 * 148;
+  int mmax = 0;
+  for (const PqrTask& t : v) mmax = std::max(mmax, t.m);
+  const bool many = (int)v.size() >= 2 * 148 || ((int)v.size() >= many_threshold() && mmax <= 400);
   for (const PqrTask& t : v) {
     if (t.m >= 128 && !many) big.push_back(t);
     else {

@@ -225,19 +225,28 @@ __global__ void lists_kernel(const long long* __restrict__ offl, int l, int d, i
 }
 
 // greedy first-fit colouring in Morton order, conflict = N(i) \ {i} (R6); one thread per level
+// greedy first-fit in Morton order (R6) is sequential by definition: one thread walks the boxes,
+// the colours live in shared memory (byte per box) when they fit
 __global__ void colour_kernel(const long long* __restrict__ offl, int nb, int ncap, const int* __restrict__ ncnt,
-                              const int* __restrict__ nidx, int* __restrict__ col) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int b = 0; b < nb; ++b) col[b] = -1;
+                              const int* __restrict__ nidx, int* __restrict__ col, int use_smem) {
+  extern __shared__ signed char cs[];
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    col[b] = -1;
+    if (use_smem) cs[b] = -1;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   for (int b = 0; b < nb; ++b) {
     if (!(offl[b + 1] > offl[b])) continue;
     unsigned long long used = 0;
     for (int t = 0; t < ncnt[b]; ++t) {
       int j = nidx[(size_t)b * ncap + t];
-      if (j != b && col[j] >= 0 && col[j] < 64) used |= 1ull << col[j];
+      const int cj = use_smem ? cs[j] : col[j];
+      if (j != b && cj >= 0 && cj < 64) used |= 1ull << cj;
     }
     int c = 0;
     while (used & (1ull << c)) ++c;
+    if (use_smem) cs[b] = (signed char)c;
     col[b] = c;
   }
 }
@@ -284,7 +293,9 @@ void tree_lists(const long long* offl, int l, int d, int ncap, int icap, int* nc
   LAUNCH(lists_kernel, grid_for(1 << (d * l)), 256, 0, s, offl, l, d, ncap, icap, ncnt, nidx, icnt, iidx);
 }
 void tree_colour(const long long* offl, int nb, int ncap, const int* ncnt, const int* nidx, int* col, cudaStream_t s) {
-  LAUNCH(colour_kernel, 1, 1, 0, s, offl, nb, ncap, ncnt, nidx, col);
+  const int use_smem = nb <= 200 * 1024;
+  if (use_smem) ensure_dyn_smem(colour_kernel, (size_t)nb);
+  LAUNCH(colour_kernel, 1, 256, use_smem ? (size_t)nb : 0, s, offl, nb, ncap, ncnt, nidx, col, use_smem);
 }
 
 }  // namespace aifmm
