@@ -216,6 +216,23 @@ __device__ __forceinline__ int block_min_int(int v, int* red) {
   return r;
 }
 
+// (sum, max) over the block in one shared-memory round
+template <int NT>
+__device__ __forceinline__ void block_sum_max(double s, double m, double* red, double* so, double* mo) {
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) { red[w] = s; red[16 + w] = m; }
+  __syncthreads();
+  double ts = 0.0, tm = -1.0;
+  for (int q = 0; q < NT / 32; ++q) { ts += red[q]; tm = fmax(tm, red[16 + q]); }
+  *so = ts;
+  *mo = tm;
+}
+
 // (max |x|, lowest index attaining it) over the block in one shared-memory round
 template <int NT>
 __device__ __forceinline__ void block_argmax(double v, int idx, double* redv, int* redi, double* mx, int* at) {
@@ -779,16 +796,15 @@ __global__ void __launch_bounds__(PQR_NT) pqr_tasks_kernel(const PqrTask* __rest
   __syncthreads();
   int t = 0, t_trunc = -1;
   while (true) {
-    double part = 0.0;
-    for (int c = tid; c < nc; c += PQR_NT) part += norms[c];
-    const double res2 = block_sum<PQR_NT>(part, red);
+    // residual ||W||_F^2 and the largest column norm in one reduction
+    double part = 0.0, v = -1.0;
+    for (int c = tid; c < nc; c += PQR_NT) { part += norms[c]; v = fmax(v, sqrt(norms[c])); }
+    double res2, mx;
+    block_sum_max<PQR_NT>(part, v, red, &res2, &mx);
     const bool ok = !(sqrt(res2) > tau);
     if (ok && t_trunc < 0) t_trunc = t;
     if (t >= tk.tmin && ok) break;
     if (t >= tk.tmax) break;
-    double v = -1.0;
-    for (int c = tid; c < nc; c += PQR_NT) v = fmax(v, sqrt(norms[c]));
-    const double mx = block_max<PQR_NT>(v, red);
     if (!(mx > 0.0)) break;
     const double thr = mx * (1.0 - TIE);
     int cand = 0x7fffffff;
@@ -903,23 +919,20 @@ pqr_cluster_kernel(const PqrTask* __restrict__ tasks, int smem_cap) {
   const int r0 = min(m, rank * rw), r1 = min(m, r0 + rw);
   int t = 0, t_trunc = -1;
   while (true) {
-    double part = 0.0;
-    for (int c = tid; c < ncl; c += PQR_NT) part += norms[c];
-    part = block_sum<PQR_NT>(part, red);
-    if (tid == 0) s_part = part;
+    // residual and largest column norm: one block reduction, one cluster barrier
+    double part = 0.0, v = -1.0;
+    for (int c = tid; c < ncl; c += PQR_NT) { part += norms[c]; v = fmax(v, sqrt(norms[c])); }
+    block_sum_max<PQR_NT>(part, v, red, &part, &v);
+    if (tid == 0) { s_part = part; s_max = v; }
     cl.sync();
-    double res2 = 0.0;
-    for (int q = 0; q < PQC; ++q) res2 += *cl.map_shared_rank(&s_part, q);
+    double res2 = 0.0, mx = -1.0;
+    for (int q = 0; q < PQC; ++q) {
+      res2 += *cl.map_shared_rank(&s_part, q);
+      mx = fmax(mx, *cl.map_shared_rank(&s_max, q));
+    }
     const bool ok = !(sqrt(res2) > tau);
     if (ok && t_trunc < 0) t_trunc = t;
     if ((t >= tk.tmin && ok) || t >= tk.tmax) break;
-    double v = -1.0;
-    for (int c = tid; c < ncl; c += PQR_NT) v = fmax(v, sqrt(norms[c]));
-    v = block_max<PQR_NT>(v, red);
-    if (tid == 0) s_max = v;
-    cl.sync();
-    double mx = -1.0;
-    for (int q = 0; q < PQC; ++q) mx = fmax(mx, *cl.map_shared_rank(&s_max, q));
     if (!(mx > 0.0)) break;
     const double thr = mx * (1.0 - TIE);
     int cand = 0x7fffffff;
@@ -1250,8 +1263,8 @@ hh_panel_cluster_smem_kernel(const HHTask* __restrict__ tasks, int j, int cap_ro
   const int cnt = hi - lo;
   double* A = tk.A + j + (size_t)j * ld;
   __shared__ double red[32];
-  __shared__ double s_sig, s_alpha;
-  __shared__ double s_dot[HHB];
+  __shared__ double s_sig[2], s_alpha[2];   // double-buffered by column parity: no trailing
+  __shared__ double s_dot[2][HHB];           // cluster barrier per column (WAR is ordered by the next column's barriers)
   __shared__ double wloc[HHB];
   __shared__ double tau_s[HHB];
   __shared__ double gram[HHB][HHB + 1];
@@ -1269,12 +1282,13 @@ hh_panel_cluster_smem_kernel(const HHTask* __restrict__ tasks, int j, int cap_ro
     double p = 0.0;
     for (int i = i0 + tid; i < cnt; i += 256) p += x[i] * x[i];
     p = block_sum<256>(p, red);
-    if (tid == 0) { s_sig = p; if (owner) s_alpha = x[c - lo]; }
+    const int ph = c & 1;
+    if (tid == 0) { s_sig[ph] = p; if (owner) s_alpha[ph] = x[c - lo]; }
     cl.sync();
     double sigma = 0.0;
-    for (int q = 0; q < HHC; ++q) sigma += *cl.map_shared_rank(&s_sig, q);
+    for (int q = 0; q < HHC; ++q) sigma += cl.map_shared_rank(s_sig, q)[ph];
     const int orank = min(HHC - 1, c / chunk);
-    const double alpha = *cl.map_shared_rank(&s_alpha, orank);
+    const double alpha = cl.map_shared_rank(s_alpha, orank)[ph];
     double tau = 0.0, beta = alpha, scal = 0.0;
     if (sigma > 0.0) {
       const double nrm = sqrt(alpha * alpha + sigma);
@@ -1290,12 +1304,12 @@ hh_panel_cluster_smem_kernel(const HHTask* __restrict__ tasks, int j, int cap_ro
       double w = (owner && lane == 0) ? y[c - lo] : 0.0;
       for (int i = i0 + lane; i < cnt; i += 32) w += x[i] * y[i];
       for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-      if (lane == 0) s_dot[cc] = w;
+      if (lane == 0) s_dot[ph][cc] = w;
     }
     cl.sync();
     for (int cc = c + 1 + tid; cc < nbw; cc += 256) {
       double w = 0.0;
-      for (int q = 0; q < HHC; ++q) w += cl.map_shared_rank(s_dot, q)[cc];
+      for (int q = 0; q < HHC; ++q) w += cl.map_shared_rank(&s_dot[0][0], q)[ph * HHB + cc];
       wloc[cc] = w * tau;
     }
     __syncthreads();
@@ -1306,8 +1320,9 @@ hh_panel_cluster_smem_kernel(const HHTask* __restrict__ tasks, int j, int cap_ro
       for (int i = i0 + lane; i < cnt; i += 32) y[i] -= w * x[i];
     }
     if (owner && tid == 0) x[c - lo] = beta;
-    cl.sync();
+    __syncthreads();
   }
+  cl.sync();
   // write back, explicit V, partial Gram
   for (int e = tid; e < cnt * nbw; e += 256) {
     const int i = e % cnt, c = e / cnt, gi = lo + i;
