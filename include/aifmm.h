@@ -149,6 +149,11 @@ int aifmm_set_timing(int on);
 /* Test hook: in-place inverse of one n x n column-major device matrix with the library's
  * batched Gauss-Jordan (R16; the kernel behind pivot inverses and the top solve). */
 int aifmm_debug_inverse(double* A, int n, int lda);
+/* Test hook: first stage of the two-stage RRQR (reading R8b) on `batch` device matrices A_b
+ * (n x m column-major, ld n, stored back to back; destroyed): M_b = R_b^T (m x min(n,m), ld m,
+ * back to back), where A_b = Q_b R_b (Householder; TSQR row chunks when n > 768 and m <= 384).
+ * R_b is unique up to the signs of its rows. */
+int aifmm_debug_tri_root(double* A, int n, int m, int batch, double* M);
 
 #ifdef __cplusplus
 }

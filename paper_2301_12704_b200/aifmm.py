@@ -22,7 +22,7 @@ SYMBOLS = ["aifmm_build", "aifmm_set_compression_tol", "aifmm_factor", "aifmm_so
            "aifmm_solve_host", "aifmm_free", "aifmm_last_error", "aifmm_set_stream",
            "aifmm_get_tree", "aifmm_get_level_offsets", "aifmm_get_lists", "aifmm_get_colours",
            "aifmm_get_ranks", "aifmm_stats", "aifmm_reset_counters", "aifmm_set_timing",
-           "aifmm_debug_inverse", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres"]
+           "aifmm_debug_inverse", "aifmm_debug_tri_root", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres"]
 STAT_NAMES = ["build_ms", "factor_ms", "solve_ms", "levels", "top_size", "factor_flops",
               "schur_flops", "schur_ms", "launches", "compressions", "max_rank", "device_bytes",
               "schur_bytes", "schur_launches", "solve_bytes", "host_syncs"]
@@ -62,6 +62,7 @@ def load(path: str = LIB_PATH):
     lib.aifmm_stats.argtypes = [P]
     lib.aifmm_set_timing.argtypes = [I]
     lib.aifmm_debug_inverse.argtypes = [P, I, I]
+    lib.aifmm_debug_tri_root.argtypes = [P, I, I, I, P]
     lib.aifmm_matvec_build.argtypes = [D]
     lib.aifmm_matvec.argtypes = [P, P, I]
     lib.aifmm_gmres.argtypes = [P, P, I, D, I, I, P, P]
@@ -192,6 +193,18 @@ def debug_inverse(M):
     Mc = M.to(torch.float64).t().contiguous()   # column-major storage of M
     _check(load().aifmm_debug_inverse(ctypes.c_void_p(Mc.data_ptr()), Mc.shape[0], Mc.shape[0]))
     return Mc.t()
+
+
+def debug_tri_root(A):
+    """R^T of the Householder / TSQR factorisation of each matrix of a (batch, n, m) CUDA float64
+    tensor (test hook; R unique up to row signs).  Returns (batch, m, min(n, m))."""
+    import torch
+    b, n, m = A.shape
+    Ac = A.to(torch.float64).transpose(1, 2).contiguous()   # column-major storage per matrix
+    r = min(n, m)
+    M = torch.empty((b, r, m), dtype=torch.float64, device=A.device)
+    _check(load().aifmm_debug_tri_root(ctypes.c_void_p(Ac.data_ptr()), n, m, b, ctypes.c_void_p(M.data_ptr())))
+    return M.transpose(1, 2)
 
 
 def matvec_build(tol: float):

@@ -113,6 +113,53 @@ struct NLevel {        // NNCA per level
   double* dU = nullptr;                // compact U (nR x k, ld nR) at Uoff
 };
 
+// Blocks of one level keyed by (row box p, column box q) with q in a per-box list of p (the near
+// list N(p) or the interaction list IL(p); fixed capacity per box, sorted by Morton id): flat
+// storage over the list slots, binary-search lookup, no hashing.
+struct BlkTable {
+  int nb = 0, cap = 0;
+  const int* cnt = nullptr;   // list length per box
+  const int* idx = nullptr;   // nb x cap list entries
+  std::vector<Blk> v;
+  std::vector<char> has;
+  void init(int nb_, int cap_, const int* cnt_, const int* idx_) {
+    nb = nb_;
+    cap = cap_;
+    cnt = cnt_;
+    idx = idx_;
+    v.assign((size_t)nb * cap, Blk{});
+    has.assign((size_t)nb * cap, 0);
+  }
+  void clear() {
+    v.clear();
+    has.clear();
+    nb = 0;
+  }
+  long long slot(long long key) const {
+    if (!nb) return -1;
+    const int p = (int)(key / nb), q = (int)(key % nb);
+    const int* L = idx + (size_t)p * cap;
+    const int* e = L + cnt[p];
+    const int* it = std::lower_bound(L, e, q);
+    return (it != e && *it == q) ? (long long)p * cap + (it - L) : -1;
+  }
+  Blk& operator[](long long key) {
+    const long long s = slot(key);
+    AIFMM_REQUIRE(s >= 0, AIFMM_ESINGULAR_PIVOT, "block outside the near/interaction lists");
+    has[s] = 1;
+    return v[s];
+  }
+  Blk& at(long long key) {
+    const long long s = slot(key);
+    AIFMM_REQUIRE(s >= 0 && has[s], AIFMM_ESINGULAR_PIVOT, "missing block");
+    return v[s];
+  }
+  Blk* get(long long key) {
+    const long long s = slot(key);
+    return (s >= 0 && has[s]) ? &v[s] : nullptr;
+  }
+};
+
 struct FLevel {
   int l = 0, nb = 0;
   std::vector<int> boxes;
@@ -121,8 +168,8 @@ struct FLevel {
   int* dinfo = nullptr;                // per-box pivot-inverse status (checked at level end)
   std::vector<double*> U, V, Ud, Vd;   // capacity: U,V m x m; Ud,Vd m x kP (ld m)
   std::vector<char> E;
-  std::unordered_map<long long, Blk> nearb;   // current version of near blocks
-  std::unordered_map<long long, Blk> A, F;    // far M2L (cap m_p x m_q), far fill (dist-2)
+  BlkTable nearb;      // current version of near blocks (over N(p))
+  BlkTable A, F;       // far M2L (cap kcap_p x kcap_q), far fill m_p x m_q (distance 2); over IL(p)
   std::set<std::pair<int, int>> pending;
   std::vector<Rec> rec;
   std::vector<int> xoff;               // row offset of child c (level l+1 id) inside its parent's x
@@ -518,9 +565,9 @@ static void setup_level(Ctx& c, int l) {
   f.rec.assign(nb, Rec{});
   DevPool& S = c.scr(l);
   S.reset();   // held level l+2 (stream order makes the reuse safe)
-  f.nearb.clear();
-  f.A.clear();
-  f.F.clear();
+  f.nearb.init(nb, c.ncap, c.ncnt[l].data(), c.nidx[l].data());
+  f.A.init(nb, c.icap, c.icnt[l].data(), c.iidx[l].data());
+  f.F.init(nb, c.icap, c.icnt[l].data(), c.iidx[l].data());
   f.pending.clear();
   const NLevel& nl = c.nn[l];
   FLevel* prev = (l < c.L) ? &c.fl[l + 1] : nullptr;
@@ -542,7 +589,7 @@ static void setup_level(Ctx& c, int l) {
     // compression grows ranks by ~1-1.5x the NNCA rank (measured); regrow() handles the rest
     f.kcap[b] = std::min(f.m[b], 2 * f.k[b] + 16);
   }
-  f.dinfo = S.i(nb);
+  f.dinfo = c.persist.i(nb);   // checked once at the end of the factorisation (no level-end sync)
   AIFMM_CUDA(cudaMemsetAsync(f.dinfo, 0, sizeof(int) * nb, c.s));
   // zero-initialised capacity storage: U, V, Ud, Vd, far A, far F
   // zero-initialised blocks are carved from the level pool; consecutive carvings are
@@ -616,8 +663,8 @@ static void setup_level(Ctx& c, int l) {
           for (int ch2 = 0; ch2 < (1 << d); ++ch2) {
             int c2 = (q << d) | ch2;
             if (!c.nonempty(l + 1, c2)) continue;
-            auto it = prev->nearb.find(prev->key(c1, c2));
-            const Blk& src = (it != prev->nearb.end()) ? it->second : prev->A.at(prev->key(c1, c2));
+            const Blk* it = prev->nearb.get(prev->key(c1, c2));
+            const Blk& src = it ? *it : prev->A.at(prev->key(c1, c2));
             cb.copy(src.p, src.ld, blk.p + (size_t)prev->xoff[c2] * blk.ld + prev->xoff[c1], blk.ld,
                     prev->k[c1], prev->k[c2]);
           }
@@ -635,7 +682,6 @@ static void setup_level(Ctx& c, int l) {
     }
   }
   g_prof.hlap("setup.plan");
-  AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
   cb.run(c.up, c.s);
   if (!kt.empty()) launch_keval(c.up.put(kt), (int)kt.size(), 4, c.pts, c.kp, c.dflag, c.s);
   g_prof.hlap("setup.launch");
@@ -760,7 +806,7 @@ static void orthonormalise(Ctx& c, FLevel& f) {
   GemmBatch g;
   // Ud <- T Ud, Vd <- T' Vd ; A_pq <- T_p A_pq T'_q^T
   std::vector<double*> udc(f.nb, nullptr), vdc(f.nb, nullptr);
-  std::unordered_map<long long, double*> tmpA;
+  std::vector<double*> tmpA((size_t)f.nb * c.icap, nullptr);   // by IL slot of (b, q)
   for (int b : f.boxes) {
     const int m = f.m[b], k = f.k[b];
     if (!k) continue;
@@ -776,7 +822,7 @@ static void orthonormalise(Ctx& c, FLevel& f) {
       int q = il[t];
       if (!f.k[q]) continue;
       double* tp = c.work.d((size_t)k * f.k[q]);
-      tmpA[f.key(b, q)] = tp;
+      tmpA[f.A.slot(f.key(b, q))] = tp;
       const Blk& a = f.A[f.key(b, q)];
       g.task(tp, k, k, f.k[q], 0.0);
       g.term(1.0, a.p, a.ld, 0, T2[q], f.k[q], 1, f.k[q]);
@@ -800,12 +846,11 @@ static void orthonormalise(Ctx& c, FLevel& f) {
       if (!f.k[q]) continue;
       const Blk& a = f.A[f.key(b, q)];
       g.task(a.p, a.ld, k, f.k[q], 0.0);
-      g.term(1.0, T[b], k, 0, tmpA[f.key(b, q)], k, 0, k);
+      g.term(1.0, T[b], k, 0, tmpA[f.A.slot(f.key(b, q))], k, 0, k);
     }
   }
   g.run(c.up, c.s, &c.fc_all);
-  c.up.sync();
-  c.work.reset();
+  c.work.reset();   // stream order: later writes to these temporaries follow the reads
 }
 
 // Far (M2L) blocks are stored with a per-box rank capacity kcap; when compression grows a box's
@@ -1063,10 +1108,13 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
     c.stats[AIFMM_STAT_COMPRESSIONS] += 1;
   }
   regrow(c, f, grown);
-  for (auto& kv : f.A) {
-    int p = (int)(kv.first / f.nb), q = (int)(kv.first % f.nb);
-    kv.second.rows = f.k[p];
-    kv.second.cols = f.k[q];
+  for (int b : aff) {   // only the compressed boxes' ranks changed
+    int ni;
+    const int* il = c.ilist(f.l, b, &ni);
+    for (int t = 0; t < ni; ++t) {
+      f.A.at(f.key(b, il[t])).rows = f.k[b];
+      f.A.at(f.key(il[t], b)).cols = f.k[b];
+    }
   }
   // redirection: A_xy += U~_x^* F_xy V~_y  (P2P) | F V~ (P2L) | U~^* F (M2P)
   GemmBatch g;
@@ -1144,39 +1192,52 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
       if (nl[t] != i) { P.nbs[a].push_back(nl[t]); P.wcol[a].push_back({nl[t], tot}); tot += live(f, nl[t]); }
     P.tot[a] = tot;
   }
-  // (p, q, a) triples sorted by target then by a (ascending eliminated box = fixed order)
-  struct Tg { long long key; int a; };
-  std::vector<Tg> tgs;
+  // targets (p, q) in ascending (p, q) order, each with its eliminated boxes a in ascending
+  // order (fixed summation order): p runs over the boxes next to the colour, a over the colour's
+  // boxes in N(p), q over N(cs[a]) \ cs[a]
+  std::vector<int> pos(f.nb, -1);
+  std::vector<char> isp(f.nb, 0);
+  for (size_t a = 0; a < cs.size(); ++a) pos[cs[a]] = (int)a;
   for (size_t a = 0; a < cs.size(); ++a)
-    for (int p : P.nbs[a])
-      for (int q : P.nbs[a]) tgs.push_back(Tg{f.key(p, q), (int)a});
-  std::sort(tgs.begin(), tgs.end(), [](const Tg& x, const Tg& y) { return x.key < y.key || (x.key == y.key && x.a < y.a); });
+    for (int p : P.nbs[a]) isp[p] = 1;
   g_prof.hlap("tg.sort");
+  std::vector<std::pair<int, int>> qa;   // (q, a) of one target row p
   std::vector<int> grp_a;
-  for (size_t t0 = 0; t0 < tgs.size();) {
-    size_t t1 = t0;
-    grp_a.clear();
-    while (t1 < tgs.size() && tgs[t1].key == tgs[t0].key) grp_a.push_back(tgs[t1++].a);
-    const int p = (int)(tgs[t0].key / f.nb), q = (int)(tgs[t0].key % f.nb);
-    t0 = t1;
-    const int M = live(f, p), N = live(f, q);
-    if (!M || !N) continue;
-    Blk T;
-    auto it = f.nearb.find(f.key(p, q));
-    if (it != f.nearb.end()) T = it->second;
-    else if (f.E[p] && f.E[q]) T = f.A.at(f.key(p, q));
-    else {
-      T = f.F.at(f.key(p, q));
-      AIFMM_REQUIRE(c.cheb(l, p, q) == 2, AIFMM_ESINGULAR_PIVOT, "fill-in outside N and IL");
-      P.new_pending.push_back({std::min(p, q), std::max(p, q)});
+  for (int p = 0; p < f.nb; ++p) {
+    if (!isp[p]) continue;
+    qa.clear();
+    int npn;
+    const int* pn = c.nlist(l, p, &npn);
+    for (int t = 0; t < npn; ++t) {
+      const int a = pos[pn[t]];
+      if (a < 0) continue;
+      for (int q : P.nbs[a]) qa.push_back({q, a});
     }
-    P.g.task(T.p, T.ld, M, N, 1.0);
-    for (int a : grp_a) {
-      const int i = cs[a];
-      if (!f.m[i]) continue;
-      const Blk& C = f.nearb.at(f.key(p, i));
-      P.fix.push_back({P.g.nterms(), a, wcol_of(P.wcol[a], q)});
-      P.g.term(-1.0, C.p, C.ld, 0, nullptr, 0, 0, f.m[i]);   // B patched in eliminate_colour
+    std::sort(qa.begin(), qa.end());
+    for (size_t t0 = 0; t0 < qa.size();) {
+      size_t t1 = t0;
+      grp_a.clear();
+      while (t1 < qa.size() && qa[t1].first == qa[t0].first) grp_a.push_back(qa[t1++].second);
+      const int q = qa[t0].first;
+      t0 = t1;
+      const int M = live(f, p), N = live(f, q);
+      if (!M || !N) continue;
+      Blk T;
+      if (const Blk* it = f.nearb.get(f.key(p, q))) T = *it;
+      else if (f.E[p] && f.E[q]) T = f.A.at(f.key(p, q));
+      else {
+        T = f.F.at(f.key(p, q));
+        AIFMM_REQUIRE(c.cheb(l, p, q) == 2, AIFMM_ESINGULAR_PIVOT, "fill-in outside N and IL");
+        P.new_pending.push_back({std::min(p, q), std::max(p, q)});
+      }
+      P.g.task(T.p, T.ld, M, N, 1.0);
+      for (int a : grp_a) {
+        const int i = cs[a];
+        if (!f.m[i]) continue;
+        const Blk& C = f.nearb.at(f.key(p, i));
+        P.fix.push_back({P.g.nterms(), a, wcol_of(P.wcol[a], q)});
+        P.g.term(-1.0, C.p, C.ld, 0, nullptr, 0, 0, f.m[i]);   // B patched in eliminate_colour
+      }
     }
   }
   g_prof.hlap("tg.tasks");
@@ -1289,13 +1350,42 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   if (g_prof.on) g_prof.end("elim.tail");
 }
 
+// The kernels record coincident points (near-field kernel blocks) and singular box pivots in
+// sticky device flags; they are read once, at the end of the factorisation or when another error
+// interrupts it (so that the root cause is the one reported), instead of synchronising the
+// stream at every level.
+static void deferred_checks(Ctx& c) {
+  check_flag(c, AIFMM_ECOINCIDENT, "coincident points with a singular kernel");
+  for (int l = c.L; l >= 2 && l < (int)c.fl.size(); --l) {
+    const FLevel& fl = c.fl[l];
+    if (!fl.dinfo) continue;
+    std::vector<int> info = d2h(c, fl.dinfo, fl.nb);
+    for (int b : fl.boxes)
+      if (info[b])
+        throw Error(AIFMM_ESINGULAR_PIVOT, "singular pivot at level " + std::to_string(l) + " box " + std::to_string(b));
+  }
+}
+
+static void factor_levels(Ctx& c);
 static void factor_all(Ctx& c) {
+  c.fl.assign(c.L + 1, FLevel{});
+  AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
+  try {
+    factor_levels(c);
+  } catch (const Error&) {
+    deferred_checks(c);
+    throw;
+  }
+}
+
+static void factor_levels(Ctx& c) {
   const int L = c.L;
-  c.fl.assign(L + 1, FLevel{});
   for (int l = L; l >= 2; --l) {
     g_prof.begin(c.s);
     setup_level(c, l);
-    check_flag(c, AIFMM_ECOINCIDENT, "coincident points with a singular kernel");
+    // the near-field kernel blocks are evaluated at the leaf level only (upper levels assemble
+    // theirs from the children's blocks): one check there
+    if (l == L) check_flag(c, AIFMM_ECOINCIDENT, "coincident points with a singular kernel");
     FLevel& f = c.fl[l];
     g_prof.end("setup");
     g_prof.begin(c.s);
@@ -1320,12 +1410,6 @@ static void factor_all(Ctx& c) {
       g_prof.end(("eliminate.L" + std::to_string(l)).c_str());
     }
     AIFMM_REQUIRE(f.pending.empty(), AIFMM_ESINGULAR_PIVOT, "pending far fill-ins at level end");
-    {
-      std::vector<int> info = d2h(c, f.dinfo, f.nb);
-      for (int b : f.boxes)
-        if (info[b])
-          throw Error(AIFMM_ESINGULAR_PIVOT, "singular pivot at level " + std::to_string(l) + " box " + std::to_string(b));
-    }
     if (g_prof.on) {
       double ms = 0, mx = 0, ks = 0, kx = 0, k0s = 0;
       for (int b : f.boxes) { ms += f.m[b]; mx = std::max(mx, (double)f.m[b]); ks += f.k[b]; kx = std::max(kx, (double)f.k[b]); k0s += c.nn[l].k[b]; }
@@ -1356,8 +1440,8 @@ static void factor_all(Ctx& c) {
   for (int p : f.boxes)
     for (int q : f.boxes) {
       if (!f.k[p] || !f.k[q]) continue;
-      auto it = f.nearb.find(f.key(p, q));
-      const Blk& B = (it != f.nearb.end()) ? it->second : f.A.at(f.key(p, q));
+      const Blk* it = f.nearb.get(f.key(p, q));
+      const Blk& B = it ? *it : f.A.at(f.key(p, q));
       cb.copy(B.p, B.ld, c.topinv + (size_t)f.zrow[q] * c.topn + f.zrow[p], c.topn, f.k[p], f.k[q]);
     }
   cb.run(c.up, c.s);
@@ -1368,6 +1452,10 @@ static void factor_all(Ctx& c) {
     int info = d2h(c, dinfo, 1)[0];
     if (info) throw Error(AIFMM_ESINGULAR_PIVOT, "singular top-level system");
   }
+  // deferred checks (the kernels set sticky device flags; reading them once here keeps the
+  // level loop free of stream synchronisations): coincident points in the near-field kernel
+  // blocks, singular box pivots
+  deferred_checks(c);
   c.stats[AIFMM_STAT_TOP_SIZE] = c.topn;
   c.work.reset();
   g_prof.end("top");
@@ -1974,6 +2062,20 @@ int aifmm_debug_inverse(double* A, int n, int lda) {
   int info = d2h(c, dinfo, 1)[0];
   c.work.reset();
   if (info) throw Error(AIFMM_ESINGULAR_PIVOT, "singular matrix");
+  CAPI_END
+}
+
+int aifmm_debug_tri_root(double* A, int n, int m, int batch, double* M) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(A && M && n >= 1 && m >= 1 && batch >= 1, AIFMM_EINVALID_ARG, "bad tri_root arguments");
+  const int r = std::min(n, m);
+  std::vector<TriRootReq> reqs;
+  for (int b = 0; b < batch; ++b)
+    reqs.push_back(TriRootReq{A + (size_t)b * n * m, n, n, m, M + (size_t)b * m * r, m});
+  batched_tri_root(reqs, c.work, c.up, c.s);
+  c.up.sync();
+  c.work.reset();
   CAPI_END
 }
 

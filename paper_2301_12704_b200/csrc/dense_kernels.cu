@@ -1138,6 +1138,209 @@ __global__ void __launch_bounds__(HHP_NT) hh_panel_kernel(const HHTask* __restri
   for (int e = tid; e < HHB * HHB; e += HHP_NT) tk.T[e] = Ts[e % HHB][e / HHB];
 }
 
+// One CTA (512 threads) per task with the whole panel (rows <= HHS_ROWS, 32 columns) staged in
+// shared memory: one load, 32 column steps at shared-memory speed, one store.  Used for the row
+// chunks of the TSQR stage (batched_tri_root), whose chunk height is chosen to fit.  Same
+// arithmetic (thread partition, reduction order) as hh_panel_kernel.
+constexpr int HHS_ROWS = 768;
+__global__ void __launch_bounds__(HHP_NT) hh_panel_smem_kernel(const HHTask* __restrict__ tasks, int j) {
+  extern __shared__ __align__(16) double hps[];   // rows x nbw, ld = rows
+  const HHTask tk = tasks[blockIdx.x];
+  const int r = min(tk.n, tk.m);
+  if (j >= r) return;
+  const int nbw = min(HHB, r - j), rows = tk.n - j, ld = tk.lda;
+  double* A = tk.A + j + (size_t)j * ld;
+  double* P = hps;
+  __shared__ double red[32];
+  __shared__ double tau_s[HHB];
+  __shared__ double G[HHB][HHB + 1];
+  __shared__ double Ts[HHB][HHB + 1];
+  constexpr int NW = HHP_NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < rows * nbw; e += HHP_NT) {
+    const int i = e % rows, c = e / rows;
+    P[(size_t)c * rows + i] = A[(size_t)c * ld + i];
+  }
+  __syncthreads();
+  for (int c = 0; c < nbw; ++c) {
+    double* x = P + (size_t)c * rows + c;
+    const int len = rows - c;
+    double p = 0.0;
+    for (int i = 1 + tid; i < len; i += HHP_NT) p += x[i] * x[i];
+    const double sigma = block_sum<HHP_NT>(p, red);
+    const double alpha = x[0];
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (sigma > 0.0) {
+      const double nrm = sqrt(alpha * alpha + sigma);
+      beta = (alpha >= 0.0) ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (sigma > 0.0)
+      for (int i = 1 + tid; i < len; i += HHP_NT) x[i] *= scal;
+    __syncthreads();
+    if (tid == 0) { x[0] = beta; tau_s[c] = tau; }
+    for (int cc = c + 1 + warp; cc < nbw; cc += NW) {
+      double* y = P + (size_t)cc * rows + c;
+      double w = (lane == 0) ? y[0] : 0.0;
+      for (int i = 1 + lane; i < len; i += 32) w += x[i] * y[i];
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      w *= tau;
+      if (lane == 0) y[0] -= w;
+      for (int i = 1 + lane; i < len; i += 32) y[i] -= w * x[i];
+    }
+    __syncthreads();
+  }
+  // write back, explicit V (ld n, unit diagonal, zeros above)
+  for (int e = tid; e < rows * nbw; e += HHP_NT) {
+    const int i = e % rows, c = e / rows;
+    const double v = P[(size_t)c * rows + i];
+    A[(size_t)c * ld + i] = v;
+    tk.V[(size_t)c * tk.n + i] = (i < c) ? 0.0 : (i == c ? 1.0 : v);
+  }
+  // Gram V^T V (a < b) from shared memory, one warp per entry
+  for (int e = warp; e < nbw * nbw; e += NW) {
+    const int a = e % nbw, b = e / nbw;
+    if (a >= b) continue;
+    const double* va = P + (size_t)a * rows;
+    const double* vb = P + (size_t)b * rows;
+    double s = 0.0;
+    for (int i = b + lane; i < rows; i += 32) s += (i == a ? 1.0 : va[i]) * (i == b ? 1.0 : vb[i]);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) G[a][b] = s;
+  }
+  for (int e = tid; e < HHB * HHB; e += HHP_NT) Ts[e % HHB][e / HHB] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < nbw; ++i) {
+    const double ti = tau_s[i];
+    if (tid < i) {
+      double s = 0.0;
+      for (int b = tid; b < i; ++b) s += Ts[tid][b] * G[b][i];
+      Ts[tid][i] = -ti * s;
+    } else if (tid == i) {
+      Ts[i][i] = ti;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < HHB * HHB; e += HHP_NT) tk.T[e] = Ts[e % HHB][e / HHB];
+}
+
+// Register-resident panel: 256 threads, thread t owns rows t + 256 q (q < RPT) of the 32-column
+// panel in registers (rows <= 256 RPT).  Column step c needs ONE 32-value block reduction:
+//   tot[k] = sum_{i>c} a_i[c] a_i[k]   (k = c: sigma; k > c: dots with the trailing columns;
+//                                       k < c: V^T v_c for the compact-WY factor T)
+// with row c broadcast through shared memory; then v_i = a_i[c] / (alpha - beta),
+// v^T y_k = a_c[k] + scal tot[k], and the rank-1 update is local to each thread.  Same
+// Householder convention (dlarfg / dlarft forward) as hh_panel_kernel; the summation order of
+// the reductions differs (butterfly within warps, then across the 8 warps).
+constexpr int HHR_NT = 256;
+__device__ __forceinline__ void warp_transpose_reduce32(double (&p)[HHB], int lane) {
+  // after it, lane l holds (in p[0]) the warp sum of value l: 16 + 8 + 4 + 2 + 1 shuffles
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int t = 0; t < off; ++t) {
+      const double send = upper ? p[t] : p[t + off];
+      const double keep = upper ? p[t + off] : p[t];
+      p[t] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+}
+template <int RPT>
+__global__ void __launch_bounds__(HHR_NT) hh_panel_reg_kernel(const HHTask* __restrict__ tasks, int j) {
+  const HHTask tk = tasks[blockIdx.x];
+  const int r = min(tk.n, tk.m);
+  if (j >= r) return;
+  const int nbw = min(HHB, r - j), rows = tk.n - j, ld = tk.lda;
+  double* A = tk.A + j + (size_t)j * ld;
+  __shared__ double red[2][HHR_NT / 32][HHB];
+  __shared__ double tot[2][HHB];
+  __shared__ double rowc[2][HHB];
+  __shared__ double Ts[HHB][HHB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double a[RPT][HHB];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = tid + HHR_NT * q;
+#pragma unroll
+    for (int k = 0; k < HHB; ++k) a[q][k] = (i < rows && k < nbw) ? A[(size_t)k * ld + i] : 0.0;
+  }
+  for (int e = tid; e < HHB * (HHB + 1); e += HHR_NT) (&Ts[0][0])[e] = 0.0;
+#pragma unroll
+  for (int c = 0; c < HHB; ++c) {
+    if (c < nbw) {
+      const int ph = c & 1;
+      if (tid == c) {
+#pragma unroll
+        for (int k = 0; k < HHB; ++k) rowc[ph][k] = a[0][k];
+      }
+      double p[HHB];
+#pragma unroll
+      for (int k = 0; k < HHB; ++k) p[k] = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = tid + HHR_NT * q;
+        const double x = (i > c && i < rows) ? a[q][c] : 0.0;
+#pragma unroll
+        for (int k = 0; k < HHB; ++k) p[k] = fma(x, a[q][k], p[k]);
+      }
+      warp_transpose_reduce32(p, lane);
+      red[ph][warp][lane] = p[0];
+      __syncthreads();
+      if (tid < HHB) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < HHR_NT / 32; ++w) t += red[ph][w][tid];
+        tot[ph][tid] = t;
+      }
+      __syncthreads();
+      const double sigma = tot[ph][c], alpha = rowc[ph][c];
+      double tau = 0.0, beta = alpha, scal = 0.0;
+      if (sigma > 0.0) {
+        const double nrm = sqrt(alpha * alpha + sigma);
+        beta = (alpha >= 0.0) ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      double tw[HHB];   // tau * v^T y_k for the trailing columns
+#pragma unroll
+      for (int k = 0; k < HHB; ++k) tw[k] = (k > c) ? tau * (rowc[ph][k] + scal * tot[ph][k]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = tid + HHR_NT * q;
+        const double v = (i > c) ? a[q][c] * scal : (i == c ? 1.0 : 0.0);
+#pragma unroll
+        for (int k = c + 1; k < HHB; ++k) a[q][k] = fma(-tw[k], v, a[q][k]);
+        if (i > c) a[q][c] = v;
+        else if (i == c) a[q][c] = beta;
+      }
+      // T[0:c, c] = -tau T[0:c, 0:c] (V^T v_c),  (V^T v_c)_b = a_c[b] + scal tot[b]
+      if (tid < c) {
+        double t = 0.0;
+        for (int b = tid; b < c; ++b) t += Ts[tid][b] * (rowc[ph][b] + scal * tot[ph][b]);
+        Ts[tid][c] = -tau * t;
+      } else if (tid == c) {
+        Ts[c][c] = tau;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = tid + HHR_NT * q;
+    if (i < rows) {
+#pragma unroll
+      for (int k = 0; k < HHB; ++k)
+        if (k < nbw) {
+          A[(size_t)k * ld + i] = a[q][k];
+          tk.V[(size_t)k * tk.n + i] = (i < k) ? 0.0 : (i == k ? 1.0 : a[q][k]);
+        }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < HHB * HHB; e += HHR_NT) tk.T[e] = Ts[e % HHB][e / HHB];
+}
+
 // Cluster variant of the panel: the 8 CTAs of a cluster split the panel rows and combine
 // their partial norms / dot products through distributed shared memory (DSMEM), so the long
 // panels of the upper levels (n up to several thousand rows) are not serialised on one SM.
@@ -1518,9 +1721,16 @@ __global__ void hh_extract_rt_kernel(const HHTask* __restrict__ tasks, double* c
   const int r = min(tk.n, tk.m);
   double* M = out[blockIdx.x];
   const int ldm = ldo[blockIdx.x];
-  for (int e = threadIdx.x; e < tk.m * r; e += blockDim.x) {
-    const int jj = e % tk.m, i = e / tk.m;   // M[jj, i] = R[i, jj]
-    M[(size_t)i * ldm + jj] = (i <= jj) ? tk.A[(size_t)jj * tk.lda + i] : 0.0;
+  if (ldm > 0) {
+    for (int e = threadIdx.x; e < tk.m * r; e += blockDim.x) {
+      const int jj = e % tk.m, i = e / tk.m;   // M[jj, i] = R[i, jj]
+      M[(size_t)i * ldm + jj] = (i <= jj) ? tk.A[(size_t)jj * tk.lda + i] : 0.0;
+    }
+  } else {                                     // ldm < 0: R itself (r x m, ld -ldm), TSQR stacking
+    for (int e = threadIdx.x; e < tk.m * r; e += blockDim.x) {
+      const int i = e % r, jj = e / r;
+      M[(size_t)jj * (-ldm) + i] = (i <= jj) ? tk.A[(size_t)jj * tk.lda + i] : 0.0;
+    }
   }
 }
 
@@ -1658,7 +1868,8 @@ void hh_make(void* out, double* A, int lda, int n, int m, double* V, double* T) 
   *static_cast<HHTask*>(out) = HHTask{A, lda, n, m, V, T};
 }
 void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode, int nmax) {
-  // mode 0: one CTA; mode 1: 8-CTA cluster (global memory); mode 2: cluster, smem-staged
+  // mode 0: one CTA; mode 1: 8-CTA cluster (global memory); mode 2: cluster, smem-staged;
+  // mode 3: one CTA, smem-staged (rows <= HHS_ROWS)
   if (mode == 2) {
     const int cap_rows = (std::max(nmax - j, 1) + HHC - 1) / HHC;
     const size_t smem = (size_t)cap_rows * HHB * sizeof(double);
@@ -1673,6 +1884,15 @@ void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode,
       AIFMM_CUDA(e);
     }
     ++g_launches;
+  } else if (mode == 4) {
+    // register-resident panel (rows - j <= 256 RPT); nmax = max rows of the batch
+    if (nmax - j <= HHR_NT) LAUNCH(hh_panel_reg_kernel<1>, ntasks, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
+    else LAUNCH(hh_panel_reg_kernel<2>, ntasks, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
+  } else if (mode == 3) {
+    // one CTA, panel in shared memory (rows - j <= HHS_ROWS)
+    const size_t smem = (size_t)std::max(std::min(nmax - j, HHS_ROWS), 1) * HHB * sizeof(double);
+    ensure_dyn_smem(hh_panel_smem_kernel, (size_t)HHS_ROWS * HHB * sizeof(double));
+    LAUNCH(hh_panel_smem_kernel, ntasks, HHP_NT, smem, s, static_cast<const HHTask*>(t), j);
   } else if (mode == 1) {
     LAUNCH(hh_panel_cluster_kernel, ntasks * HHC, 256, 0, s, static_cast<const HHTask*>(t), j);
   } else {

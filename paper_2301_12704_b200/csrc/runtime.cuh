@@ -478,10 +478,43 @@ struct TriRootReq {
   double* out;
   int ldm;
 };
+constexpr int HH_SMEM_ROWS = 768;   // = HHS_ROWS of hh_panel_smem_kernel
+constexpr int HH_REG_ROWS = 512;    // = 256 threads x 2 rows of hh_panel_reg_kernel<2>
 template <class Pool>
-inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Uploader& up, cudaStream_t s,
+inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work, Uploader& up, cudaStream_t s,
                              FlopCounter* fc = nullptr) {
-  if (reqs.empty()) return;
+  if (reqs_in.empty()) return;
+  // TSQR: a tall request (n > HH_REG_ROWS rows) is split into balanced row chunks of at most
+  // HH_REG_ROWS rows.  Each chunk's R (min(n_c, m) x m upper trapezoid) goes into a stacked
+  // buffer, rows in chunk order, and the stack is factored in turn (recursively; a split is only
+  // made when the stack has <= 0.8 n rows): R([A_1; A_2; ...]) = R([R_1; R_2; ...]) up to the
+  // signs of its rows, which the pivoted QR of the second stage (on R^T's columns) does not see.
+  // Every chunk panel then lives in registers (hh_panel_reg_kernel).
+  static const bool no_tsqr = getenv("AIFMM_NO_TSQR") != nullptr;   // debug toggle
+  static const int tsqr_mmax = getenv("AIFMM_TSQR_MMAX") ? atoi(getenv("AIFMM_TSQR_MMAX")) : 128;
+  std::vector<TriRootReq> reqs, stacks;
+  for (const TriRootReq& q : reqs_in) {
+    bool split = !no_tsqr && q.m >= 1 && q.m <= tsqr_mmax && q.n > HH_REG_ROWS;
+    int nch = 0, S = 0;
+    if (split) {
+      nch = (q.n + HH_REG_ROWS - 1) / HH_REG_ROWS;
+      for (int c = 0; c < nch; ++c) S += std::min(q.n / nch + (c < q.n % nch ? 1 : 0), q.m);
+      split = 5LL * S <= 4LL * q.n;
+    }
+    if (!split) {
+      reqs.push_back(q);
+      continue;
+    }
+    double* st = work.d((size_t)S * q.m);
+    int row0 = 0, srow = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int nc = q.n / nch + (c < q.n % nch ? 1 : 0);
+      reqs.push_back(TriRootReq{q.A + row0, q.lda, nc, q.m, st + srow, -S});
+      row0 += nc;
+      srow += std::min(nc, q.m);
+    }
+    stacks.push_back(TriRootReq{st, S, S, q.m, q.out, q.ldm});
+  }
   const size_t tsz = hh_task_size();
   // long panels (n >= 512 rows) go to the 8-CTA cluster kernel, short ones to one CTA
   // three classes: short panels (one CTA), long panels staged in the smem of an 8-CTA cluster,
@@ -495,12 +528,19 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
   for (const auto& q : reqs) nmax_rows = std::max(nmax_rows, q.n);
   const bool many = !hh_cluster && ((int)reqs.size() >= 2 * 148 ||
                                     ((int)reqs.size() >= many_threshold() && nmax_rows <= 4096));
-  for (const auto& q : reqs) if (q.n < 512 || many) sorted_reqs.push_back(q);
-  const size_t nsmall = sorted_reqs.size();
+  // classes: panels that fit one CTA's shared memory; other short or many panels (one CTA,
+  // global memory); long panels staged in the smem of an 8-CTA cluster; very long (cluster, global)
+  int nmax_rg = 0, nmax_sm = 0;
+  for (const auto& q : reqs) if (q.n <= HH_REG_ROWS) { sorted_reqs.push_back(q); nmax_rg = std::max(nmax_rg, q.n); }
+  const size_t nrg = sorted_reqs.size();
+  for (const auto& q : reqs) if (q.n > HH_REG_ROWS && q.n <= HH_SMEM_ROWS) { sorted_reqs.push_back(q); nmax_sm = std::max(nmax_sm, q.n); }
+  const size_t nsm = sorted_reqs.size() - nrg;
+  for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && (q.n < 512 || many)) sorted_reqs.push_back(q);
+  const size_t nsmall = sorted_reqs.size() - nrg - nsm;
   int nmax_mid = 0;
-  for (const auto& q : reqs) if (!many && q.n >= 512 && q.n <= SM_ROWS) { sorted_reqs.push_back(q); nmax_mid = std::max(nmax_mid, q.n); }
-  const size_t nmid = sorted_reqs.size() - nsmall;
-  for (const auto& q : reqs) if (!many && q.n > SM_ROWS) sorted_reqs.push_back(q);
+  for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && !many && q.n >= 512 && q.n <= SM_ROWS) { sorted_reqs.push_back(q); nmax_mid = std::max(nmax_mid, q.n); }
+  const size_t nmid = sorted_reqs.size() - nrg - nsm - nsmall;
+  for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && !many && q.n > SM_ROWS) sorted_reqs.push_back(q);
   const std::vector<TriRootReq>& R = sorted_reqs;
   std::vector<char> tb(tsz * reqs.size());
   std::vector<double*> V(reqs.size()), T(reqs.size());
@@ -524,10 +564,13 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
   if (g_prof.on) { g_prof.end("cmp.proj"); g_prof.begin(s); }
   for (int j = 0; j < rmax; j += HH_PANEL) {
     if (g_prof.on) g_prof.begin(s);
-    if (nsmall) launch_hh_panel(dt, (int)nsmall, j, s, 0, 0);
-    if (nmid) launch_hh_panel(static_cast<const char*>(dt) + nsmall * tsz, (int)nmid, j, s, 2, nmax_mid);
-    if (reqs.size() > nsmall + nmid)
-      launch_hh_panel(static_cast<const char*>(dt) + (nsmall + nmid) * tsz, (int)(reqs.size() - nsmall - nmid), j, s, 1, 0);
+    const char* d0 = static_cast<const char*>(dt);
+    const size_t o1 = nrg, o2 = o1 + nsm, o3 = o2 + nsmall, o4 = o3 + nmid;
+    if (nrg && j < nmax_rg) launch_hh_panel(d0, (int)nrg, j, s, 4, nmax_rg);
+    if (nsm && j < nmax_sm) launch_hh_panel(d0 + o1 * tsz, (int)nsm, j, s, 3, nmax_sm);
+    if (nsmall) launch_hh_panel(d0 + o2 * tsz, (int)nsmall, j, s, 0, 0);
+    if (nmid) launch_hh_panel(d0 + o3 * tsz, (int)nmid, j, s, 2, nmax_mid);
+    if (reqs.size() > o4) launch_hh_panel(d0 + o4 * tsz, (int)(reqs.size() - o4), j, s, 1, 0);
     // fused trailing update: one CTA per (task, 64-column block of the trailing matrix)
     std::vector<int2> ut;
     for (size_t i = 0; i < reqs.size(); ++i) {
@@ -544,6 +587,7 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs, Pool& work, Up
   }
   if (g_prof.on) g_prof.begin(s);
   launch_hh_extract(dt, (int)reqs.size(), douts, dldo, s);
+  if (!stacks.empty()) batched_tri_root(stacks, work, up, s, fc);   // next TSQR round
 }
 // run pivoted-QR tasks: tall ones (m >= 128) on 8-CTA clusters, the rest one CTA each
 inline void run_pqr(const std::vector<PqrTask>& v, Uploader& up, cudaStream_t s) {

@@ -1,7 +1,10 @@
 """GPU unit checks of the batched dense kernels behind the hot path, against plain numpy
 float64 references: the Gauss-Jordan pivot inverse (reading R16) in its three variants —
 shared-memory (n <= 160), blocked single-CTA panels, blocked 8-CTA cluster panels (few large
-matrices: the top system) — on saddle-point matrices [[K, U], [V^T, 0]] that need pivoting."""
+matrices: the top system) — on saddle-point matrices [[K, U], [V^T, 0]] that need pivoting; and the first stage of the
+two-stage RRQR (reading R8b: R of a tall W^T) in each of its routes — one-CTA shared-memory
+panels, TSQR row chunks over one or several rounds, one-CTA / cluster global-memory panels —
+against numpy's Householder R (unique up to row signs) and the Gram identity R^T R = A^T A."""
 import numpy as np
 import pytest
 
@@ -45,3 +48,35 @@ def test_singular_pivot_reported():
     with pytest.raises(G.AIFMMError) as e:
         G.debug_inverse(torch.from_numpy(P).cuda())
     assert e.value.code == -5
+
+
+@pytest.mark.parametrize("n,m,batch,rank", [
+    (200, 16, 3, None),      # register panel, one row per thread
+    (300, 40, 2, None),      # register panel, two rows per thread; two panels
+    (700, 32, 2, None),      # TSQR: 2 chunks -> 64-row stack
+    (700, 400, 1, None),     # no split (stack would not shrink): shared-memory panel
+    (2000, 64, 3, None),     # TSQR: 4 chunks -> 256-row stack
+    (2000, 64, 2, 20),       # rank-deficient (fill-in-like), TSQR
+    (5000, 100, 1, None),    # TSQR over three rounds (1000 -> 200 rows)
+    (1700, 300, 2, None),    # TSQR rounds 1200 -> 900 -> 600, then shared-memory panels
+    (1500, 500, 2, None),    # m > 384: one-CTA global-memory / cluster panels
+    (6000, 450, 1, None),    # very long panels (cluster)
+])
+def test_tri_root_householder_and_tsqr(n, m, batch, rank):
+    rng = np.random.default_rng(n + m)
+    A = rng.standard_normal((batch, n, m))
+    if rank is not None:
+        A = np.einsum("bnr,brm->bnm", rng.standard_normal((batch, n, rank)), rng.standard_normal((batch, rank, m)))
+    MT = G.debug_tri_root(torch.from_numpy(A).cuda()).cpu().numpy()   # (batch, m, r) = R^T
+    for b in range(batch):
+        R = MT[b].T
+        r = min(n, m)
+        assert R.shape == (r, m)
+        assert np.all(np.tril(R, -1) == 0.0)
+        nA = np.linalg.norm(A[b])
+        # Gram identity (holds for any R of A, rank-deficient or not)
+        assert np.linalg.norm(R.T @ R - A[b].T @ A[b]) <= 1e-13 * nA * nA
+        if rank is None:   # full rank: R unique up to row signs
+            Rn = np.linalg.qr(A[b], mode="r")
+            D = np.sign(np.diag(R)) * np.sign(np.diag(Rn))
+            assert np.linalg.norm(D[:, None] * R - Rn) <= 1e-12 * nA

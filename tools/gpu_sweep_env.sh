@@ -1,0 +1,7 @@
+#!/bin/bash
+# factor time of configs 2 and 3 under debug toggles of the compression stage
+for env in "X=1" "AIFMM_NO_TSQR=1" "AIFMM_TSQR_MMAX=64" "AIFMM_TSQR_MMAX=128" "AIFMM_TSQR_MMAX=200"; do
+  for cfg in 1 2; do
+    echo "$env cfg$cfg $(env $env timeout 600 python tools/gpu_perf.py $cfg 2>/dev/null | grep '^{' | tail -1 | cut -c1-150)"
+  done
+done
