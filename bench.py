@@ -196,7 +196,7 @@ def run_ours(args, cfg):
     clocks.start()
     A.reset_counters()
     tb = tf = ts = 0.0
-    schur_ms = schur_flops = 0.0
+    schur_ms = schur_flops = schur_bytes = schur_launches = 0.0
     launches = 0.0
     for _ in range(args.steps):
         flush.fill_(1.0)
@@ -209,6 +209,8 @@ def run_ours(args, cfg):
         st = A.stats()
         schur_ms += st["schur_ms"]
         schur_flops += st["schur_flops"]
+        schur_bytes += st["schur_bytes"]
+        schur_launches += st["schur_launches"]
         launches += st["launches"]
         A.reset_counters()
     if world > 1:
@@ -251,11 +253,24 @@ def run_ours(args, cfg):
     pk = _peaks()
     achieved = (schur_flops / (schur_ms / 1e3)) / 1e12 if schur_ms > 0 else None
     peak = pk.get("fp64_dgemm_tflops") or (pk["bf16_tflops"] * 45.0 / 2250.0 if pk["bf16_tflops"] else None)
+    # DRAM traffic per Schur launch from the committed `ncu --set full` capture of exactly these
+    # launches (NVTX range "schur"; tools/ncu_kernel_traffic.py), next to the algorithmic bytes
+    traffic, ncu_src = None, None
+    try:
+        nc = json.load(open(os.path.join(ROOT, "profiles", "r01_schur_gemm_ncu.json")))
+        traffic, ncu_src = nc.get("dram_bytes_per_launch"), nc
+    except Exception:
+        pass
     roof = {
         "kernel": "gemm_tasks_kernel (Schur-complement updates, DMMA)",
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": (achieved / peak) if (achieved and peak) else None,
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_source": ("profiles/r01_schur_gemm_ncu.json: mean dram__bytes_read.sum + dram__bytes_write.sum "
+                           "over %d captured Schur launches" % ncu_src["launches_captured"]) if ncu_src else None,
+        "algorithmic_bytes_per_launch": (schur_bytes / schur_launches) if schur_launches else None,
+        "algorithmic_flop_per_launch": (schur_flops / schur_launches) if schur_launches else None,
+        "launches_per_step": schur_launches / args.steps,
         "peak_source": "cuBLAS FP64 DGEMM 8192^3 measured on this pool (profiles/r01_fp64_dgemm_peak.json); "
                        "bf16 measured x 45/2250 nominal ratio = %.1f" % (pk["bf16_tflops"] * 45.0 / 2250.0 if pk["bf16_tflops"] else float("nan")),
         "schur_ms_per_step": schur_ms / args.steps, "schur_gflop_per_step": schur_flops / args.steps / 1e9,

@@ -78,8 +78,13 @@ class Level:
 class AIFMM:
     """Oracle AIFMM: build (tree, lists, colours, NNCA), factor, solve."""
 
-    def __init__(self, points, kernel_id, kparams, leaf_size, tol, tol_c=None, nnca_eps=None):
+    def __init__(self, points, kernel_id, kparams, leaf_size, tol, tol_c=None, nnca_eps=None, symmetric=True):
         self.kid, self.kp = kernel_id, tuple(kparams)
+        # reading R27: every kernel here is symmetric (A_ij = A_ji, targets = sources, P:1248), so
+        # the column-side fill-ins are the transposes of the row-side ones (F_pb^T = F_bp) and
+        # the V-side basis extension equals the U-side one in exact arithmetic; computing it
+        # once keeps V_b = U_b exactly (symmetric pivots [[K, U], [U^T, 0]]).
+        self.symmetric = symmetric
         self.tol = tol
         self.tol_c = tol if tol_c is None else tol_c
         self.tree = Tree(points, leaf_size)
@@ -189,16 +194,22 @@ class AIFMM:
             ps = sorted(part[b])
             m, k = lv.m[b], lv.k[b]
             FU = np.concatenate([lv.F[(b, q)] for q in ps], axis=1)       # row X_b
-            FV = np.concatenate([lv.F[(p, b)].T for p in ps], axis=1)     # column x_b
-            nU, nV = np.linalg.norm(FU), np.linalg.norm(FV)
+            nU = np.linalg.norm(FU)
             WU = tri_root(FU - lv.U[b] @ (lv.U[b].T @ FU))
-            WV = tri_root(FV - lv.V[b] @ (lv.V[b].T @ FV))
             cap = m - k
             _, tU = pivoted_qr_extend(WU, lv.U[b], self.tol_c * nU, 0, cap)
-            _, tV = pivoted_qr_extend(WV, lv.V[b], self.tol_c * nV, 0, cap)
-            tt = max(tU, tV)
-            QU = extend_basis(WU, lv.U[b], self.tol_c * nU, tt)
-            QV = extend_basis(WV, lv.V[b], self.tol_c * nV, tt)
+            if self.symmetric:                                              # R27
+                tt = tU
+                QU = extend_basis(WU, lv.U[b], self.tol_c * nU, tt)
+                QV = QU
+            else:
+                FV = np.concatenate([lv.F[(p, b)].T for p in ps], axis=1)     # column x_b
+                nV = np.linalg.norm(FV)
+                WV = tri_root(FV - lv.V[b] @ (lv.V[b].T @ FV))
+                _, tV = pivoted_qr_extend(WV, lv.V[b], self.tol_c * nV, 0, cap)
+                tt = max(tU, tV)
+                QU = extend_basis(WU, lv.U[b], self.tol_c * nU, tt)
+                QV = extend_basis(WV, lv.V[b], self.tol_c * nV, tt)
             newU[b] = np.concatenate([lv.U[b], QU], axis=1)
             newV[b] = np.concatenate([lv.V[b], QV], axis=1)
             self.stats["compressions"] += 1

@@ -11,6 +11,7 @@
 //            far fill-ins (§3.2.1-3.2.3), batched pivot inverses and Schur updates (P:724-729,
 //            Table 4); top dense solve
 //   solve  : Algorithm 4 replaying the records on nrhs columns.
+#include <nvtx3/nvToolsExt.h>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -197,6 +198,7 @@ struct Ctx {
   long long n = 0;
   KernelParams kp{};
   double tol = 0, tol_c = -1, tol_c_user = -1;
+  bool symmetric = true;                   // reading R27: V-side bases reuse the U-side ones
   double* pts = nullptr;                   // sorted points (device)
   int* perm = nullptr;                     // device int32
   int* dflag = nullptr;                    // device int error flag
@@ -899,6 +901,8 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
   std::vector<NormTask> nt;
   AIFMM_CUDA(cudaMemsetAsync(dt, 0, sizeof(int) * 4 * na, c.s));
   std::vector<char> full(na, 0);
+  // symmetric (R27): only the U side is compressed; V_b's new columns are copies of U_b's
+  const bool sym = c.symmetric;
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
     const int m = f.m[b];
@@ -911,20 +915,26 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     for (int q : part[b]) nu += live(f, q);
     su[a].n = sv[a].n = nu;
     su[a].WT = c.work.d((size_t)std::max(nu, 1) * m);
-    sv[a].WT = c.work.d((size_t)std::max(nu, 1) * m);
     su[a].r = sv[a].r = std::min(nu, m);
     su[a].M = c.work.d((size_t)m * std::max(su[a].r, 1));
-    sv[a].M = c.work.d((size_t)m * std::max(sv[a].r, 1));
+    if (!sym) {
+      sv[a].WT = c.work.d((size_t)std::max(nu, 1) * m);
+      sv[a].M = c.work.d((size_t)m * std::max(sv[a].r, 1));
+    } else {
+      sv[a].n = 0;
+    }
     int o = 0;
     for (int q : part[b]) {
       const Blk& fb = f.F.at(f.key(b, q));   // row X_b, column of q: m x live_q -> transposed
       cb.copy(fb.p, fb.ld, su[a].WT + o, nu, live(f, q), m, 1.0, /*trans=*/1);
-      const Blk& gb = f.F.at(f.key(q, b));   // row of q, column x_b: live_q x m (already W^T rows)
-      cb.copy(gb.p, gb.ld, sv[a].WT + o, nu, live(f, q), m);
+      if (!sym) {
+        const Blk& gb = f.F.at(f.key(q, b));   // row of q, column x_b: live_q x m (already W^T rows)
+        cb.copy(gb.p, gb.ld, sv[a].WT + o, nu, live(f, q), m);
+      }
       o += live(f, q);
     }
     nt.push_back(NormTask{su[a].WT, std::max(nu, 1), nu, m, dnorm + 2 * a});
-    nt.push_back(NormTask{sv[a].WT, std::max(nu, 1), nu, m, dnorm + 2 * a + 1});
+    if (!sym) nt.push_back(NormTask{sv[a].WT, std::max(nu, 1), nu, m, dnorm + 2 * a + 1});
   }
   cb.run(c.up, c.s);
   launch_norm(c.up.put(nt), (int)nt.size(), c.s);
@@ -937,9 +947,10 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     const int m = f.m[b], k = f.k[b], nu = su[a].n;
     if (!k || !nu) continue;
     tu[a] = c.work.d((size_t)nu * k);
-    tv[a] = c.work.d((size_t)nu * k);
     g.task(tu[a], nu, nu, k, 0.0);
     g.term(1.0, su[a].WT, nu, 0, f.U[b], m, 0, m);
+    if (sym) continue;
+    tv[a] = c.work.d((size_t)nu * k);
     g.task(tv[a], nu, nu, k, 0.0);
     g.term(1.0, sv[a].WT, nu, 0, f.V[b], m, 0, m);
   }
@@ -950,6 +961,7 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     if (!k || !nu) continue;
     g.task(su[a].WT, nu, nu, m, 1.0);
     g.term(-1.0, tu[a], nu, 0, f.U[b], m, 1, k);
+    if (sym) continue;
     g.task(sv[a].WT, nu, nu, m, 1.0);
     g.term(-1.0, tv[a], nu, 0, f.V[b], m, 1, k);
   }
@@ -961,7 +973,7 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     const int m = f.m[b], nu = su[a].n;
     if (!nu || !m) continue;
     tr.push_back(TriRootReq{su[a].WT, nu, nu, m, su[a].M, m});
-    tr.push_back(TriRootReq{sv[a].WT, nu, nu, m, sv[a].M, m});
+    if (!sym) tr.push_back(TriRootReq{sv[a].WT, nu, nu, m, sv[a].M, m});
   }
   batched_tri_root(tr, c.work, c.up, c.s, &c.fc_all);
   if (g_prof.on) { g_prof.end("cmp.proj+triroot"); g_prof.begin(c.s); }
@@ -979,13 +991,29 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     const int m = f.m[b], k = f.k[b];
     if (full[a]) continue;
     pq.push_back(PqrTask{wu[a].W, f.U[b], m, m, m, wu[a].nc, k, 0, m - k, 0, dnorm + 2 * a, c.tol_c, dt + 4 * a, dt + 4 * a + 1});
-    pq.push_back(PqrTask{wv[a].W, f.V[b], m, m, m, wv[a].nc, k, 0, m - k, 0, dnorm + 2 * a + 1, c.tol_c, dt + 4 * a + 2, dt + 4 * a + 3});
+    if (!sym)
+      pq.push_back(PqrTask{wv[a].W, f.V[b], m, m, m, wv[a].nc, k, 0, m - k, 0, dnorm + 2 * a + 1, c.tol_c, dt + 4 * a + 2, dt + 4 * a + 3});
     smem = std::max(smem, (size_t)std::max(wu[a].nc, wv[a].nc) + m + m);
   }
   if (!pq.empty()) run_pqr(pq, c.up, c.s);
   std::vector<int> th = d2h(c, dt, 4 * na);
   if (g_prof.on) { g_prof.end("cmp.pqrA"); g_prof.begin(c.s); }
   tgt.assign(na, 0);
+  if (sym) {
+    // one side: the truncation rank is the new rank (tmin = 0, so the columns taken are exactly
+    // the t_trunc of R8); V_b's new columns are U_b's
+    CopyBatch vb;
+    for (int a = 0; a < na; ++a) {
+      int b = aff[a];
+      const int m = f.m[b], k = f.k[b];
+      if (full[a]) continue;
+      tgt[a] = std::min(th[4 * a + 1], m - k);
+      vb.copy(f.U[b] + (size_t)k * m, m, f.V[b] + (size_t)k * m, m, m, tgt[a]);
+    }
+    vb.run(c.up, c.s);
+    if (g_prof.on) { g_prof.end("cmp.pqrB"); g_prof.begin(c.s); }
+    return;
+  }
   std::vector<int> hu(na), hv(na);
   pq.clear();
   smem = 0;
@@ -1266,6 +1294,22 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   }
   cb.run(c.up, c.s);
   batched_inverse(inv, c.work, c.up, c.s, &c.fc_all);
+  static const bool dbg_piv = getenv("AIFMM_DEBUG_PIVOTS") != nullptr;   // debug: largest |P_i^-1| entries
+  if (dbg_piv) {
+    std::vector<std::pair<double, int>> mx;
+    for (int i : cs) {
+      const int n = f.m[i] + f.k[i];
+      if (!n) continue;
+      std::vector<double> h = d2h(c, f.rec[i].G, (size_t)n * n);
+      double a = 0.0;
+      for (double v : h) a = std::max(a, std::fabs(v));
+      mx.push_back({a, i});
+    }
+    std::sort(mx.rbegin(), mx.rend());
+    for (size_t t = 0; t < std::min<size_t>(3, mx.size()); ++t)
+      fprintf(stderr, "[aifmm pivots] level %d colour-first-box %d box %d m %d k %d max|G| %.3e\n", l, cs[0], mx[t].second,
+              f.m[mx[t].second], f.k[mx[t].second], mx[t].first);
+  }
   if (g_prof.on) { g_prof.end("elim.inverse"); g_prof.begin(c.s); }
   // 2. W_i = G[:, 0:m] * R_i (row X_i blocks), columns ordered as N(i) \ i
   std::vector<double*> W(cs.size());
@@ -1336,7 +1380,9 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   }
   if (g_prof.on) { g_prof.end("elim.plan"); g_prof.begin(c.s); }
   long long l0 = g_launches;
+  nvtxRangePushA("schur");   // lets `ncu --nvtx --nvtx-include schur/` capture exactly these launches
   P.g.run(c.up, c.s, &c.fc_schur);
+  nvtxRangePop();
   c.stats[AIFMM_STAT_SCHUR_LAUNCHES] += (double)(g_launches - l0);
   if (c.timing) {
     AIFMM_CUDA(cudaEventRecord(e1, c.s));
@@ -1875,6 +1921,7 @@ int aifmm_factor(void) {
     throw Error(AIFMM_ESTATE, "already factored: call aifmm_build again");
   }
   c.tol_c = (c.tol_c_user >= 0) ? c.tol_c_user : c.tol;
+  c.symmetric = getenv("AIFMM_ASYMMETRIC") == nullptr;   // R27 (debug toggle: independent U/V sides)
   for (auto& e : c.ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   c.ev.clear();
   factor_all(c);

@@ -75,9 +75,11 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmTerm* __restrict
     return t;
   };
   int nk = 0;                                // number of (term, k0) tiles of this task
+  bool has_add = false;                      // addition terms (A == nullptr: C += alpha B)
   for (int t = tk.term_begin; t < tk.term_end; ++t) {
     const GemmTerm tm = terms[t];
     if (tm.A) nk += (tm.K + BK - 1) / BK;
+    else has_add = true;
   }
   int lt = next_term(tk.term_begin), lk = 0; // next tile to load
   auto load_next = [&](int st) {
@@ -132,27 +134,45 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmTerm* __restrict
     __syncthreads();
   }
   cp_async_wait<0>();
-  // epilogue: C = beta*C + acc + sum(addition terms)
+  // epilogue: C = beta*C + (acc + sum(addition terms)).  Every load (C, addition terms) is
+  // issued before the first store: the compiler cannot prove that a store to C does not alias a
+  // later load, and would otherwise expose one memory latency per element.
+  // Done per 8-row group i (8 elements per thread) to bound the registers.
+  const bool has_beta = tk.beta != 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int gm = m0 + wm + i * 8 + (lane >> 2);
+    const bool okm = gm < tk.M;
+    double cv[4][2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int gn = n0 + wn + j * 8 + (lane & 3) * 2 + e;
-        if (gm < tk.M && gn < tk.N) {
-          double v = acc[i][j][e];
-          for (int t = tk.term_begin; t < tk.term_end; ++t) {
-            const GemmTerm tm = terms[t];
-            if (tm.A != nullptr) continue;
-            v += tm.alpha * (tm.transB ? tm.B[(size_t)gm * tm.ldb + gn] : tm.B[(size_t)gn * tm.ldb + gm]);
+        cv[j][e] = (has_beta && okm && gn < tk.N) ? tk.C[(size_t)gn * tk.ldc + gm] : 0.0;
+      }
+    if (has_add) {
+      for (int t = tk.term_begin; t < tk.term_end; ++t) {
+        const GemmTerm tm = terms[t];
+        if (tm.A != nullptr) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int gn = n0 + wn + j * 8 + (lane & 3) * 2 + e;
+            if (okm && gn < tk.N)
+              acc[i][j][e] += tm.alpha * (tm.transB ? tm.B[(size_t)gm * tm.ldb + gn] : tm.B[(size_t)gn * tm.ldb + gm]);
           }
-          double* c = tk.C + (size_t)gn * tk.ldc + gm;
-          *c = (tk.beta == 0.0) ? v : tk.beta * (*c) + v;
-        }
       }
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gn = n0 + wn + j * 8 + (lane & 3) * 2 + e;
+        if (okm && gn < tk.N)
+          tk.C[(size_t)gn * tk.ldc + gm] = has_beta ? tk.beta * cv[j][e] + acc[i][j][e] : acc[i][j][e];
+      }
   }
 }
 

@@ -45,16 +45,20 @@ ks = sorted([(e.time_range.start, e.time_range.end, e.name) for e in evs], key=l
 busy = 0.0
 cur_s = cur_e = None
 gaps = []
+prev_nm = ''
 for s, e, nm in ks:
+    if cur_e is not None and e > cur_e:
+        pass
     if cur_e is None:
         cur_s, cur_e = s, e
         continue
     if s > cur_e:
         busy += cur_e - cur_s
-        gaps.append((s - cur_e, nm))
+        gaps.append((s - cur_e, prev_nm.split('(')[0][:40] + ' -> ' + nm.split('(')[0][:40]))
         cur_s, cur_e = s, e
     else:
         cur_e = max(cur_e, e)
+    prev_nm = nm
 if cur_e is not None:
     busy += cur_e - cur_s
 span = ks[-1][1] - ks[0][0] if ks else 0
@@ -71,8 +75,8 @@ for k, (t, c) in sorted(tot.items(), key=lambda x: -x[1][0])[:30]:
     print(f"{t / 1e3:10.2f} ms {c:6d}  {k}")
 gaps.sort(key=lambda x: -x[0])
 print("largest idle gaps (us, next kernel):")
-for g, nm in gaps[:25]:
-    print(f"{g:10.1f}  {nm[:70]}")
+for g, nm in gaps[:40]:
+    print(f"{g:10.1f}  {nm[:90]}")
 hist = [0, 0, 0, 0, 0]
 hsum = [0.0] * 5
 for g, _ in gaps:
