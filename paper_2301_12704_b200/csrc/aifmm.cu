@@ -23,6 +23,7 @@
 namespace aifmm {
 
 long long g_launches = 0;
+void (*g_before_launch)() = nullptr;
 
 // tree launchers
 void tree_minmax(const double* pts, long long n, int d, double* part, int nparts, int* nonfinite, double* root, cudaStream_t s);
@@ -159,6 +160,13 @@ struct BlkTable {
     const long long s = slot(key);
     return (s >= 0 && has[s]) ? &v[s] : nullptr;
   }
+  // entry t of box p's list (no search)
+  Blk& put_at(int p, int t) {
+    const size_t s = (size_t)p * cap + t;
+    has[s] = 1;
+    return v[s];
+  }
+  Blk& at_slot(int p, int t) { return v[(size_t)p * cap + t]; }
 };
 
 struct FLevel {
@@ -245,6 +253,7 @@ static Ctx& ctx() {
     AIFMM_CUDA(cudaStreamCreateWithFlags(&g_ctx->s, cudaStreamNonBlocking));
     g_ctx->own_stream = true;
     g_ctx->up.init(g_ctx->s);
+    g_before_launch = [] { if (g_ctx) g_ctx->up.flush(); };
     AIFMM_CUDA(cudaMalloc(&g_ctx->dflag, 64));
   }
   return *g_ctx;
@@ -377,7 +386,7 @@ static void build_nnca(Ctx& c, std::vector<NLevel>& nnv, double eps, DevPool& po
         if (l == L) ic.push_back(ICopyTask{nullptr, nl.dR + nl.Roff[b], nl.nR[b], (int)c.off[l][b]});
         else ic.push_back(ICopyTask{nnv[l + 1].dsk + nnv[l + 1].skoff[(size_t)b << c.d], nl.dR + nl.Roff[b], nl.nR[b], 0});
       }
-      if (!ic.empty()) LAUNCH(icopy_tasks_kernel, (int)ic.size(), 128, 0, c.s, c.up.put(ic));
+      if (!ic.empty()) { const ICopyTask* dic = c.up.put(ic); LAUNCH(icopy_tasks_kernel, (int)ic.size(), 128, 0, c.s, dic); }
     }
     // far sources per box (R11b): IL boxes' points at the leaf level, their children's
     // skeletons above.  Both are ranges of one index array: the identity at the leaves, the
@@ -494,7 +503,7 @@ static void build_nnca(Ctx& c, std::vector<NLevel>& nnv, double eps, DevPool& po
         ic.push_back(ICopyTask{drp + pivoff[b], nl.dsk + nl.skoff[b], nl.k[b], 0});
         ic.push_back(ICopyTask{dcp + pivoff[b], nl.dfp + nl.skoff[b], nl.k[b], 0});
       }
-      if (!ic.empty()) LAUNCH(icopy_tasks_kernel, (int)ic.size(), 128, 0, c.s, c.up.put(ic));
+      if (!ic.empty()) { const ICopyTask* dic = c.up.put(ic); LAUNCH(icopy_tasks_kernel, (int)ic.size(), 128, 0, c.s, dic); }
     }
     // operators: [A(fp,sk) | A(fp,R)] -> [I | X] by Gauss-Jordan (a solve, not an explicit
     // inverse: A(fp,sk) can be ill-conditioned), U = X^T (R10: V = U)
@@ -616,8 +625,8 @@ static void setup_level(Ctx& c, int l) {
     const int* il = c.ilist(l, b, &ni);
     for (int t = 0; t < ni; ++t) {
       int q = il[t];
-      f.A[f.key(b, q)] = Blk{carve((size_t)f.kcap[b] * f.kcap[q]), std::max(f.kcap[b], 1), f.k[b], f.k[q]};
-      if (c.cheb(l, b, q) == 2) f.F[f.key(b, q)] = Blk{carve((size_t)f.m[b] * f.m[q]), std::max(f.m[b], 1), 0, 0};
+      f.A.put_at(b, t) = Blk{carve((size_t)f.kcap[b] * f.kcap[q]), std::max(f.kcap[b], 1), f.k[b], f.k[q]};
+      if (c.cheb(l, b, q) == 2) f.F.put_at(b, t) = Blk{carve((size_t)f.m[b] * f.m[q]), std::max(f.m[b], 1), 0, 0};
     }
   }
   for (auto& r : zr) AIFMM_CUDA(cudaMemsetAsync(r.first, 0, r.second, c.s));
@@ -655,7 +664,7 @@ static void setup_level(Ctx& c, int l) {
       // the diagonal block is consumed by the pivot; off-diagonal ones are solve records
       DevPool& bp = (q == b) ? S : c.persist;
       Blk blk{bp.d(std::max<size_t>((size_t)m * f.m[q], 1)), std::max(m, 1), m, f.m[q]};
-      f.nearb[f.key(b, q)] = blk;
+      f.nearb.put_at(b, t) = blk;
       if (l == c.L) {
         kt.push_back(KEvalTask{blk.p, blk.ld, m, f.m[q], nullptr, nullptr, (int)c.off[l][b], (int)c.off[l][q]});
       } else {
@@ -678,7 +687,7 @@ static void setup_level(Ctx& c, int l) {
     const int* il = c.ilist(l, b, &ni);
     for (int t = 0; t < ni; ++t) {
       int q = il[t];
-      const Blk& a = f.A[f.key(b, q)];
+      const Blk& a = f.A.at_slot(b, t);
       if (f.k[b] && f.k[q])
         kt.push_back(KEvalTask{a.p, a.ld, f.k[b], f.k[q], nl.dsk + nl.skoff[b], nl.dsk + nl.skoff[q], 0, 0});
     }
@@ -824,8 +833,8 @@ static void orthonormalise(Ctx& c, FLevel& f) {
       int q = il[t];
       if (!f.k[q]) continue;
       double* tp = c.work.d((size_t)k * f.k[q]);
-      tmpA[f.A.slot(f.key(b, q))] = tp;
-      const Blk& a = f.A[f.key(b, q)];
+      tmpA[(size_t)b * c.icap + t] = tp;
+      const Blk& a = f.A.at_slot(b, t);
       g.task(tp, k, k, f.k[q], 0.0);
       g.term(1.0, a.p, a.ld, 0, T2[q], f.k[q], 1, f.k[q]);
     }
@@ -846,9 +855,9 @@ static void orthonormalise(Ctx& c, FLevel& f) {
     for (int t = 0; t < ni; ++t) {
       int q = il[t];
       if (!f.k[q]) continue;
-      const Blk& a = f.A[f.key(b, q)];
+      const Blk& a = f.A.at_slot(b, t);
       g.task(a.p, a.ld, k, f.k[q], 0.0);
-      g.term(1.0, T[b], k, 0, tmpA[f.A.slot(f.key(b, q))], k, 0, k);
+      g.term(1.0, T[b], k, 0, tmpA[(size_t)b * c.icap + t], k, 0, k);
     }
   }
   g.run(c.up, c.s, &c.fc_all);
@@ -1140,7 +1149,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
     int ni;
     const int* il = c.ilist(f.l, b, &ni);
     for (int t = 0; t < ni; ++t) {
-      f.A.at(f.key(b, il[t])).rows = f.k[b];
+      f.A.at_slot(b, t).rows = f.k[b];
       f.A.at(f.key(il[t], b)).cols = f.k[b];
     }
   }
@@ -1329,9 +1338,10 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   }
   g.run(c.up, c.s, &c.fc_all);
   if (g_prof.on) { g_prof.end("elim.W"); g_prof.begin(c.s); }
-  // 3. Schur updates (planned), then the new blocks (p,i) = C G12, (i,q) = G21 R = W_z,
-  //    (i,i) = -G22 (R17)
-  g_prof.hstart();
+  // 3. Schur updates (planned) are launched first; the new blocks (p,i) = C G12,
+  //    (i,q) = G21 R = W_z, (i,i) = -G22 (R17) are planned while they run (they touch no
+  //    Schur target: (p,i) with i in the colour is never a target of the colour, whose boxes
+  //    are not neighbours)
   for (const auto& fx : P.fix) {
     const int n = f.m[cs[fx.a]] + f.k[cs[fx.a]];
     GemmTerm& t = P.g.term_ref(fx.term);
@@ -1339,6 +1349,24 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     t.ldb = n;
   }
   for (auto& pr : P.new_pending) f.pending.insert(pr);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c.timing) {
+    AIFMM_CUDA(cudaEventCreate(&e0));
+    AIFMM_CUDA(cudaEventCreate(&e1));
+    AIFMM_CUDA(cudaEventRecord(e0, c.s));
+  }
+  long long l0 = g_launches;
+  nvtxRangePushA("schur");   // lets `ncu --nvtx --nvtx-include schur/` capture exactly these launches
+  P.g.run(c.up, c.s, &c.fc_schur);
+  nvtxRangePop();
+  c.stats[AIFMM_STAT_SCHUR_LAUNCHES] += (double)(g_launches - l0);
+  if (c.timing) {
+    AIFMM_CUDA(cudaEventRecord(e1, c.s));
+    c.ev.push_back({e0, e1});
+  }
+  if (g_prof.on) { g_prof.end("elim.schur"); g_prof.begin(c.s); }
+  g_prof.hstart();
+  GemmBatch gf;
   std::vector<std::pair<long long, Blk>> fresh;
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];
@@ -1352,8 +1380,8 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
       DevPool& bp = f.E[p] ? c.scr(l) : c.persist;
       Blk nb_{bp.d(std::max<size_t>((size_t)live(f, p) * k, 1)), std::max(live(f, p), 1), live(f, p), k};
       if (live(f, p) && k) {
-        P.g.task(nb_.p, nb_.ld, live(f, p), k, 0.0);
-        if (m) P.g.term(1.0, C.p, C.ld, 0, r.G + (size_t)m * n, n, 0, m);
+        gf.task(nb_.p, nb_.ld, live(f, p), k, 0.0);
+        if (m) gf.term(1.0, C.p, C.ld, 0, r.G + (size_t)m * n, n, 0, m);
       }
       fresh.push_back({f.key(p, i), nb_});
     }
@@ -1372,24 +1400,9 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     fresh.push_back({f.key(i, i), nb_});
   }
   g_prof.hlap("fresh");
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (c.timing) {
-    AIFMM_CUDA(cudaEventCreate(&e0));
-    AIFMM_CUDA(cudaEventCreate(&e1));
-    AIFMM_CUDA(cudaEventRecord(e0, c.s));
-  }
-  if (g_prof.on) { g_prof.end("elim.plan"); g_prof.begin(c.s); }
-  long long l0 = g_launches;
-  nvtxRangePushA("schur");   // lets `ncu --nvtx --nvtx-include schur/` capture exactly these launches
-  P.g.run(c.up, c.s, &c.fc_schur);
-  nvtxRangePop();
-  c.stats[AIFMM_STAT_SCHUR_LAUNCHES] += (double)(g_launches - l0);
-  if (c.timing) {
-    AIFMM_CUDA(cudaEventRecord(e1, c.s));
-    c.ev.push_back({e0, e1});
-  }
+  gf.run(c.up, c.s, &c.fc_all);
   cb.run(c.up, c.s);
-  if (g_prof.on) { g_prof.end("elim.schur"); g_prof.begin(c.s); }
+  if (g_prof.on) { g_prof.end("elim.fresh"); g_prof.begin(c.s); }
   for (auto& fr : fresh) f.nearb[fr.first] = fr.second;
   for (int i : cs) f.E[i] = 1;
   c.work.reset();   // stream order: the next colour's temporaries are written after these reads

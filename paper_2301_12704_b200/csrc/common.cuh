@@ -33,9 +33,14 @@ struct Error : public std::runtime_error {
 // Launch bookkeeping: every kernel launch of the library goes through LAUNCH so that
 // aifmm_stats can report how many of OUR kernels ran (bench "gpu_launches").
 extern long long g_launches;
+// Called before every kernel launch: uploads task lists staged since the previous launch in one
+// host-to-device copy (Uploader::flush in the library context).  LAUNCH calls it before its
+// arguments are evaluated, so a launch argument must never stage an upload itself.
+extern void (*g_before_launch)();
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                \
   do {                                                                \
     if ((grid) > 0) {                                                 \
+      if (::aifmm::g_before_launch) ::aifmm::g_before_launch();       \
       kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);     \
       AIFMM_CUDA(cudaGetLastError());                                 \
       ++::aifmm::g_launches;                                          \

@@ -1841,6 +1841,7 @@ void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s) {
 void launch_gj_unscramble(const void* t, int ntasks, int nmax, cudaStream_t s) {
   if (ntasks <= 0) return;
   dim3 grid(ntasks, (nmax + 127) / 128);
+  if (g_before_launch) g_before_launch();
   gj_unscramble_kernel<<<grid, 128, 0, s>>>(static_cast<const GJBTask*>(t));
   AIFMM_CUDA(cudaGetLastError());
   ++g_launches;
@@ -1868,6 +1869,7 @@ void launch_keval(const KEvalTask* t, int ntasks, int ysplit, const double* pts,
                   cudaStream_t s) {
   if (ntasks <= 0) return;
   dim3 g(ntasks, ysplit);
+  if (g_before_launch) g_before_launch();
   keval_tasks_kernel<<<g, 256, 0, s>>>(t, pts, kp, flag);
   AIFMM_CUDA(cudaGetLastError());
   ++g_launches;
@@ -1876,6 +1878,7 @@ void launch_keval(const KEvalTask* t, int ntasks, int ysplit, const double* pts,
 void launch_copy(const CopyTask* t, int ntasks, int ysplit, cudaStream_t s) {
   if (ntasks <= 0) return;
   dim3 g(ntasks, ysplit);
+  if (g_before_launch) g_before_launch();
   copy_tasks_kernel<<<g, 256, 0, s>>>(t);
   AIFMM_CUDA(cudaGetLastError());
   ++g_launches;
@@ -1894,6 +1897,7 @@ void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode,
     const int cap_rows = (std::max(nmax - j, 1) + HHC - 1) / HHC;
     const size_t smem = (size_t)cap_rows * HHB * sizeof(double);
     ensure_dyn_smem(hh_panel_cluster_smem_kernel, smem);
+    if (g_before_launch) g_before_launch();
     hh_panel_cluster_smem_kernel<<<ntasks * HHC, 256, smem, s>>>(static_cast<const HHTask*>(t), j, cap_rows);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

@@ -210,7 +210,7 @@ class Uploader {
     if (d_) cudaFree(d_);
     h_ = nullptr;
     d_ = nullptr;
-    cap_ = used_ = 0;
+    cap_ = used_ = flushed_ = 0;
   }
   template <class T>
   T* put(const T* src, size_t n) {
@@ -222,10 +222,16 @@ class Uploader {
       if (need > cap_) grow(std::max(need, cap_ * 2));
     }
     std::memcpy(h_ + used_, src, bytes);
-    AIFMM_CUDA(cudaMemcpyAsync(d_ + used_, h_ + used_, bytes, cudaMemcpyHostToDevice, s_));
     T* out = reinterpret_cast<T*>(d_ + used_);
     used_ += need;
-    return out;
+    return out;   // copied to the device by the next flush() (before the next kernel launch)
+  }
+  // one host-to-device copy of everything staged since the last flush
+  void flush() {
+    if (used_ > flushed_) {
+      AIFMM_CUDA(cudaMemcpyAsync(d_ + flushed_, h_ + flushed_, used_ - flushed_, cudaMemcpyHostToDevice, s_));
+      flushed_ = used_;
+    }
   }
   template <class T>
   T* put(const std::vector<T>& v) { return put(v.data(), v.size()); }
@@ -237,24 +243,25 @@ class Uploader {
     if (bytes > cap_) grow(std::max(bytes, cap_ * 2));
   }
   void sync() {
+    flush();
     AIFMM_CUDA(cudaStreamSynchronize(s_));
-    used_ = 0;
+    used_ = flushed_ = 0;
     ++syncs;
   }
   long long syncs = 0;
 
  private:
   void grow(size_t cap) {
-    if (h_) { AIFMM_CUDA(cudaStreamSynchronize(s_)); cudaFreeHost(h_); cudaFree(d_); }
+    if (h_) { flush(); AIFMM_CUDA(cudaStreamSynchronize(s_)); cudaFreeHost(h_); cudaFree(d_); }
     AIFMM_CUDA(cudaMallocHost(&h_, cap));
     AIFMM_CUDA(cudaMalloc(&d_, cap));
     cap_ = cap;
-    used_ = 0;
+    used_ = flushed_ = 0;
   }
   cudaStream_t s_ = 0;
   char* h_ = nullptr;
   char* d_ = nullptr;
-  size_t cap_ = 0, used_ = 0;
+  size_t cap_ = 0, used_ = 0, flushed_ = 0;
 };
 
 // ---------------------------------------------------------------------------------- batches
