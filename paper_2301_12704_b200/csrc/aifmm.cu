@@ -631,66 +631,88 @@ static void setup_level(Ctx& c, int l) {
   }
   for (auto& r : zr) AIFMM_CUDA(cudaMemsetAsync(r.first, 0, r.second, c.s));
   g_prof.hlap("setup.carve");
-  // fills
-  CopyBatch cb;
-  std::vector<KEvalTask> kt;
+  // near blocks: allocated serially (the pools are not thread-safe) ...
   for (int b : f.boxes) {
-    const int m = f.m[b], k = f.k[b];
-    if (l == c.L) {
-      cb.copy(nl.dU + nl.Uoff[b], nl.nR[b], f.U[b], m, m, k);
-      cb.copy(nl.dU + nl.Uoff[b], nl.nR[b], f.V[b], m, m, k);
-    } else {
-      for (int ch = 0; ch < (1 << d); ++ch) {
-        int cbx = (b << d) | ch;
-        if (!c.nonempty(l + 1, cbx)) continue;
-        cb.copy(prev->Ud[cbx], std::max(prev->m[cbx], 1), f.U[b] + prev->xoff[cbx], m, prev->k[cbx], k);
-        cb.copy(prev->Vd[cbx], std::max(prev->m[cbx], 1), f.V[b] + prev->xoff[cbx], m, prev->k[cbx], k);
-      }
-    }
-    if (l > 2) {
-      // L2L / M2M: rows of the parent's NNCA operator belonging to b
-      const int P = b >> d;
-      const NLevel& pl = c.nn[l - 1];
-      int r0 = 0;
-      for (int ch = 0; ch < (b & ((1 << d) - 1)); ++ch) r0 += nl.k[(P << d) | ch];
-      cb.copy(pl.dU + pl.Uoff[P] + r0, pl.nR[P], f.Ud[b], std::max(m, 1), k, f.kP[b]);
-      cb.copy(pl.dU + pl.Uoff[P] + r0, pl.nR[P], f.Vd[b], std::max(m, 1), k, f.kP[b]);
-    }
-    // near blocks (current version = X_p x x_q)
+    const int m = f.m[b];
     int nn_;
     const int* nbl = c.nlist(l, b, &nn_);
     for (int t = 0; t < nn_; ++t) {
-      int q = nbl[t];
+      const int q = nbl[t];
       // the diagonal block is consumed by the pivot; off-diagonal ones are solve records
       DevPool& bp = (q == b) ? S : c.persist;
-      Blk blk{bp.d(std::max<size_t>((size_t)m * f.m[q], 1)), std::max(m, 1), m, f.m[q]};
-      f.nearb.put_at(b, t) = blk;
+      f.nearb.put_at(b, t) = Blk{bp.d(std::max<size_t>((size_t)m * f.m[q], 1)), std::max(m, 1), m, f.m[q]};
+    }
+  }
+  g_prof.hlap("setup.nearalloc");
+  // ... the fill tasks are planned on several threads (box chunks, merged in box order)
+  std::vector<CopyBatch> cbt(8);
+  std::vector<std::vector<KEvalTask>> ktt(8);
+  const int nthr = parallel_chunks((int)f.boxes.size(), 256, [&](int lo, int hi, int th) {
+    CopyBatch& cb = cbt[th];
+    std::vector<KEvalTask>& kt = ktt[th];
+    for (int bi = lo; bi < hi; ++bi) {
+      const int b = f.boxes[bi];
+      const int m = f.m[b], k = f.k[b];
       if (l == c.L) {
-        kt.push_back(KEvalTask{blk.p, blk.ld, m, f.m[q], nullptr, nullptr, (int)c.off[l][b], (int)c.off[l][q]});
+        cb.copy(nl.dU + nl.Uoff[b], nl.nR[b], f.U[b], m, m, k);
+        cb.copy(nl.dU + nl.Uoff[b], nl.nR[b], f.V[b], m, m, k);
       } else {
         for (int ch = 0; ch < (1 << d); ++ch) {
-          int c1 = (b << d) | ch;
-          if (!c.nonempty(l + 1, c1)) continue;
-          for (int ch2 = 0; ch2 < (1 << d); ++ch2) {
-            int c2 = (q << d) | ch2;
-            if (!c.nonempty(l + 1, c2)) continue;
-            const Blk* it = prev->nearb.get(prev->key(c1, c2));
-            const Blk& src = it ? *it : prev->A.at(prev->key(c1, c2));
-            cb.copy(src.p, src.ld, blk.p + (size_t)prev->xoff[c2] * blk.ld + prev->xoff[c1], blk.ld,
-                    prev->k[c1], prev->k[c2]);
+          int cbx = (b << d) | ch;
+          if (!c.nonempty(l + 1, cbx)) continue;
+          cb.copy(prev->Ud[cbx], std::max(prev->m[cbx], 1), f.U[b] + prev->xoff[cbx], m, prev->k[cbx], k);
+          cb.copy(prev->Vd[cbx], std::max(prev->m[cbx], 1), f.V[b] + prev->xoff[cbx], m, prev->k[cbx], k);
+        }
+      }
+      if (l > 2) {
+        // L2L / M2M: rows of the parent's NNCA operator belonging to b
+        const int P = b >> d;
+        const NLevel& pl = c.nn[l - 1];
+        int r0 = 0;
+        for (int ch = 0; ch < (b & ((1 << d) - 1)); ++ch) r0 += nl.k[(P << d) | ch];
+        cb.copy(pl.dU + pl.Uoff[P] + r0, pl.nR[P], f.Ud[b], std::max(m, 1), k, f.kP[b]);
+        cb.copy(pl.dU + pl.Uoff[P] + r0, pl.nR[P], f.Vd[b], std::max(m, 1), k, f.kP[b]);
+      }
+      // near blocks (current version = X_p x x_q)
+      int nn_;
+      const int* nbl = c.nlist(l, b, &nn_);
+      for (int t = 0; t < nn_; ++t) {
+        const int q = nbl[t];
+        const Blk& blk = f.nearb.at_slot(b, t);
+        if (l == c.L) {
+          kt.push_back(KEvalTask{blk.p, blk.ld, m, f.m[q], nullptr, nullptr, (int)c.off[l][b], (int)c.off[l][q]});
+        } else {
+          for (int ch = 0; ch < (1 << d); ++ch) {
+            int c1 = (b << d) | ch;
+            if (!c.nonempty(l + 1, c1)) continue;
+            for (int ch2 = 0; ch2 < (1 << d); ++ch2) {
+              int c2 = (q << d) | ch2;
+              if (!c.nonempty(l + 1, c2)) continue;
+              const Blk* it = prev->nearb.get(prev->key(c1, c2));
+              const Blk& src = it ? *it : prev->A.at(prev->key(c1, c2));
+              cb.copy(src.p, src.ld, blk.p + (size_t)prev->xoff[c2] * blk.ld + prev->xoff[c1], blk.ld,
+                      prev->k[c1], prev->k[c2]);
+            }
           }
         }
       }
+      // M2L A(sk b, sk q)
+      int ni;
+      const int* il = c.ilist(l, b, &ni);
+      for (int t = 0; t < ni; ++t) {
+        const int q = il[t];
+        const Blk& a = f.A.at_slot(b, t);
+        if (f.k[b] && f.k[q])
+          kt.push_back(KEvalTask{a.p, a.ld, f.k[b], f.k[q], nl.dsk + nl.skoff[b], nl.dsk + nl.skoff[q], 0, 0});
+      }
     }
-    // M2L A(sk b, sk q)
-    int ni;
-    const int* il = c.ilist(l, b, &ni);
-    for (int t = 0; t < ni; ++t) {
-      int q = il[t];
-      const Blk& a = f.A.at_slot(b, t);
-      if (f.k[b] && f.k[q])
-        kt.push_back(KEvalTask{a.p, a.ld, f.k[b], f.k[q], nl.dsk + nl.skoff[b], nl.dsk + nl.skoff[q], 0, 0});
-    }
+  });
+  g_prof.hlap("setup.par");
+  CopyBatch cb;
+  std::vector<KEvalTask> kt;
+  for (int t = 0; t < nthr; ++t) {
+    cb.append(cbt[t]);
+    kt.insert(kt.end(), ktt[t].begin(), ktt[t].end());
   }
   g_prof.hlap("setup.plan");
   cb.run(c.up, c.s);
@@ -912,6 +934,7 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
   std::vector<char> full(na, 0);
   // symmetric (R27): only the U side is compressed; V_b's new columns are copies of U_b's
   const bool sym = c.symmetric;
+  g_prof.hstart();
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
     const int m = f.m[b];
@@ -945,6 +968,7 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     nt.push_back(NormTask{su[a].WT, std::max(nu, 1), nu, m, dnorm + 2 * a});
     if (!sym) nt.push_back(NormTask{sv[a].WT, std::max(nu, 1), nu, m, dnorm + 2 * a + 1});
   }
+  g_prof.hlap("cmp.gather");
   cb.run(c.up, c.s);
   launch_norm(c.up.put(nt), (int)nt.size(), c.s);
   if (g_prof.on) { g_prof.end("cmp.gather"); g_prof.begin(c.s); }
@@ -1154,6 +1178,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
     }
   }
   // redirection: A_xy += U~_x^* F_xy V~_y  (P2P) | F V~ (P2L) | U~^* F (M2P)
+  g_prof.hstart();
   GemmBatch g;
   CopyBatch cb;
   std::vector<std::pair<std::pair<int, int>, double*>> p2p;
@@ -1188,6 +1213,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
       }
       cb.fill(F.p, F.ld, live(f, x), live(f, y), 0.0);
     }
+  g_prof.hlap("cmp.redirect");
   g.run(c.up, c.s, &c.fc_all);
   cb.run(c.up, c.s);
   for (auto& pr : S) f.pending.erase(pr);
@@ -2133,7 +2159,7 @@ int aifmm_debug_tri_root(double* A, int n, int m, int batch, double* M) {
   std::vector<TriRootReq> reqs;
   for (int b = 0; b < batch; ++b)
     reqs.push_back(TriRootReq{A + (size_t)b * n * m, n, n, m, M + (size_t)b * m * r, m});
-  batched_tri_root(reqs, c.work, c.up, c.s);
+  batched_tri_root(reqs, c.work, c.up, c.s, nullptr, 1 << 30);   // every route, TSQR included
   c.up.sync();
   c.work.reset();
   CAPI_END

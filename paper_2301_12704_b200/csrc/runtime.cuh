@@ -1,5 +1,6 @@
 // runtime.cuh — host-side runtime pieces of libaifmm: device pools, task upload arena, batch builders.
 #pragma once
+#include <thread>
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -385,6 +386,22 @@ class GemmBatch {
   DevPool* splitk_ = nullptr;
 };
 
+// Host planning loops over boxes: contiguous chunks on up to 8 threads (serial for small n).
+// fn(lo, hi, t) must only write thread-private outputs (merged by the caller in chunk order).
+template <class F>
+inline int parallel_chunks(int n, int min_per_thread, F&& fn) {
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int T = std::max(1, std::min({8, hw, n / std::max(min_per_thread, 1)}));
+  if (T == 1) {
+    fn(0, n, 0);
+    return 1;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t) th.emplace_back([&, t] { fn((int)((long long)n * t / T), (int)((long long)n * (t + 1) / T), t); });
+  for (auto& x : th) x.join();
+  return T;
+}
+
 class CopyBatch {
  public:
   void copy(const double* src, int lds, double* dst, int ldd, int rows, int cols, double alpha = 1.0, int trans = 0,
@@ -395,6 +412,10 @@ class CopyBatch {
   }
   void fill(double* dst, int ldd, int rows, int cols, double value) { copy(nullptr, 0, dst, ldd, rows, cols, value); }
   bool empty() const { return v_.empty(); }
+  void append(const CopyBatch& o) {   // o's tasks after this batch's (order preserved)
+    v_.insert(v_.end(), o.v_.begin(), o.v_.end());
+    maxel_ = std::max(maxel_, o.maxel_);
+  }
   void run(Uploader& up, cudaStream_t s) {
     if (v_.empty()) return;
     int ys = (int)std::min<long long>(64, std::max<long long>(1, maxel_ / 4096));
@@ -489,7 +510,7 @@ constexpr int HH_SMEM_ROWS = 768;   // = HHS_ROWS of hh_panel_smem_kernel
 constexpr int HH_REG_ROWS = 512;    // = 256 threads x 2 rows of hh_panel_reg_kernel<2>
 template <class Pool>
 inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work, Uploader& up, cudaStream_t s,
-                             FlopCounter* fc = nullptr) {
+                             FlopCounter* fc = nullptr, int tsqr_m = -1) {
   if (reqs_in.empty()) return;
   // TSQR: a tall request (n > HH_REG_ROWS rows) is split into balanced row chunks of at most
   // HH_REG_ROWS rows.  Each chunk's R (min(n_c, m) x m upper trapezoid) goes into a stacked
@@ -498,7 +519,10 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   // signs of its rows, which the pivoted QR of the second stage (on R^T's columns) does not see.
   // Every chunk panel then lives in registers (hh_panel_reg_kernel).
   static const bool no_tsqr = getenv("AIFMM_NO_TSQR") != nullptr;   // debug toggle
-  static const int tsqr_mmax = getenv("AIFMM_TSQR_MMAX") ? atoi(getenv("AIFMM_TSQR_MMAX")) : 128;
+  // off by default in the factorisation (measured: no gain on configs 2 and 3); the test hook
+  // aifmm_debug_tri_root enables it for every m
+  static const int tsqr_env = getenv("AIFMM_TSQR_MMAX") ? atoi(getenv("AIFMM_TSQR_MMAX")) : 0;
+  const int tsqr_mmax = tsqr_m >= 0 ? tsqr_m : tsqr_env;
   std::vector<TriRootReq> reqs, stacks;
   for (const TriRootReq& q : reqs_in) {
     bool split = !no_tsqr && q.m >= 1 && q.m <= tsqr_mmax && q.n > HH_REG_ROWS;
@@ -594,7 +618,7 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   }
   if (g_prof.on) g_prof.begin(s);
   launch_hh_extract(dt, (int)reqs.size(), douts, dldo, s);
-  if (!stacks.empty()) batched_tri_root(stacks, work, up, s, fc);   // next TSQR round
+  if (!stacks.empty()) batched_tri_root(stacks, work, up, s, fc, tsqr_m);   // next TSQR round
 }
 // run pivoted-QR tasks: tall ones (m >= 128) on 8-CTA clusters, the rest one CTA each
 inline void run_pqr(const std::vector<PqrTask>& v, Uploader& up, cudaStream_t s) {
