@@ -1254,6 +1254,7 @@ __global__ void __launch_bounds__(HHP_NT) hh_panel_smem_kernel(const HHTask* __r
 // Householder convention (dlarfg / dlarft forward) as hh_panel_kernel; the summation order of
 // the reductions differs (butterfly within warps, then across the 8 warps).
 constexpr int HHR_NT = 256;
+constexpr int HHC_REG = 8;   // CTAs per cluster of hh_panel_reg_cluster_kernel
 __device__ __forceinline__ void warp_transpose_reduce32(double (&p)[HHB], int lane) {
   // after it, lane l holds (in p[0]) the warp sum of value l: 16 + 8 + 4 + 2 + 1 shuffles
 #pragma unroll
@@ -1468,6 +1469,125 @@ hh_panel_cluster_kernel(const HHTask* __restrict__ tasks, int j) {
     }
   }
   cl.sync();
+}
+
+// Register-resident panel on an 8-CTA cluster: CTA r of the cluster owns the contiguous row
+// slice [r*chunk, (r+1)*chunk) of the panel (chunk <= 256 RPT), one row per thread and slot, in
+// registers.  Per column: the 32-value reduction of hh_panel_reg_kernel inside each CTA, one
+// cluster barrier, then every CTA sums the 8 partial vectors and reads row c from its owner
+// through distributed shared memory (double-buffered by column parity, so one barrier per
+// column suffices).  Panels of up to 8 x 256 RPT rows.
+template <int RPT>
+__global__ void __cluster_dims__(HHC_REG, 1, 1) __launch_bounds__(HHR_NT)
+hh_panel_reg_cluster_kernel(const HHTask* __restrict__ tasks, int j) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const HHTask tk = tasks[blockIdx.x / HHC_REG];
+  const int r = min(tk.n, tk.m);
+  if (j >= r) return;                       // uniform over the cluster
+  const int nbw = min(HHB, r - j), rows = tk.n - j, ld = tk.lda;
+  const int chunk = (rows + HHC_REG - 1) / HHC_REG;
+  const int lo = min(rows, rank * chunk), hi = min(rows, lo + chunk);
+  double* A = tk.A + j + (size_t)j * ld;
+  __shared__ double red[2][HHR_NT / 32][HHB];
+  __shared__ double part[2][HHB];          // this CTA's partial sums (read remotely)
+  __shared__ double rowc[2][HHB];          // row c, if this CTA owns it (read remotely)
+  __shared__ double tot[2][HHB];
+  __shared__ double rc[2][HHB];
+  __shared__ double Ts[HHB][HHB + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double a[RPT][HHB];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = lo + tid + HHR_NT * q;
+#pragma unroll
+    for (int k = 0; k < HHB; ++k) a[q][k] = (i < hi && k < nbw) ? A[(size_t)k * ld + i] : 0.0;
+  }
+  for (int e = tid; e < HHB * (HHB + 1); e += HHR_NT) (&Ts[0][0])[e] = 0.0;
+#pragma unroll
+  for (int c = 0; c < HHB; ++c) {
+    if (c < nbw) {
+      const int ph = c & 1;
+      const int oc = min(HHC_REG - 1, c / max(chunk, 1));   // owner CTA of row c
+#pragma unroll
+      for (int q = 0; q < RPT; ++q)
+        if (lo + tid + HHR_NT * q == c) {
+#pragma unroll
+          for (int k = 0; k < HHB; ++k) rowc[ph][k] = a[q][k];
+        }
+      double p[HHB];
+#pragma unroll
+      for (int k = 0; k < HHB; ++k) p[k] = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = lo + tid + HHR_NT * q;
+        const double x = (i > c && i < hi) ? a[q][c] : 0.0;
+#pragma unroll
+        for (int k = 0; k < HHB; ++k) p[k] = fma(x, a[q][k], p[k]);
+      }
+      warp_transpose_reduce32(p, lane);
+      red[ph][warp][lane] = p[0];
+      __syncthreads();
+      if (tid < HHB) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < HHR_NT / 32; ++w) t += red[ph][w][tid];
+        part[ph][tid] = t;
+      }
+      cl.sync();
+      if (tid < HHB) {
+        double t = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < HHC_REG; ++qq) t += cl.map_shared_rank(&part[0][0], qq)[ph * HHB + tid];
+        tot[ph][tid] = t;
+        rc[ph][tid] = cl.map_shared_rank(&rowc[0][0], oc)[ph * HHB + tid];
+      }
+      __syncthreads();
+      const double sigma = tot[ph][c], alpha = rc[ph][c];
+      double tau = 0.0, beta = alpha, scal = 0.0;
+      if (sigma > 0.0) {
+        const double nrm = sqrt(alpha * alpha + sigma);
+        beta = (alpha >= 0.0) ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      double tw[HHB];
+#pragma unroll
+      for (int k = 0; k < HHB; ++k) tw[k] = (k > c) ? tau * (rc[ph][k] + scal * tot[ph][k]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) {
+        const int i = lo + tid + HHR_NT * q;
+        const double v = (i > c) ? a[q][c] * scal : (i == c ? 1.0 : 0.0);
+#pragma unroll
+        for (int k = c + 1; k < HHB; ++k) a[q][k] = fma(-tw[k], v, a[q][k]);
+        if (i > c) a[q][c] = v;
+        else if (i == c) a[q][c] = beta;
+      }
+      if (tid < c) {
+        double t = 0.0;
+        for (int b = tid; b < c; ++b) t += Ts[tid][b] * (rc[ph][b] + scal * tot[ph][b]);
+        Ts[tid][c] = -tau * t;
+      } else if (tid == c) {
+        Ts[c][c] = tau;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = lo + tid + HHR_NT * q;
+    if (i < hi) {
+#pragma unroll
+      for (int k = 0; k < HHB; ++k)
+        if (k < nbw) {
+          A[(size_t)k * ld + i] = a[q][k];
+          tk.V[(size_t)k * tk.n + i] = (i < k) ? 0.0 : (i == k ? 1.0 : a[q][k]);
+        }
+    }
+  }
+  __syncthreads();
+  if (rank == 0)
+    for (int e = tid; e < HHB * HHB; e += HHR_NT) tk.T[e] = Ts[e % HHB][e / HHB];
+  cl.sync();   // remote shared memory stays alive until every CTA has read it
 }
 
 // Same cluster panel with the panel rows of every CTA staged in shared memory (one load,
@@ -1908,6 +2028,11 @@ void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode,
       AIFMM_CUDA(e);
     }
     ++g_launches;
+  } else if (mode == 5) {
+    // register-resident panel on 8-CTA clusters (rows - j <= 8 x 256 RPT)
+    const int chunk = (std::max(nmax - j, 1) + HHC_REG - 1) / HHC_REG;
+    if (chunk <= HHR_NT) LAUNCH(hh_panel_reg_cluster_kernel<1>, ntasks * HHC_REG, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
+    else LAUNCH(hh_panel_reg_cluster_kernel<2>, ntasks * HHC_REG, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
   } else if (mode == 4) {
     // register-resident panel (rows - j <= 256 RPT); nmax = max rows of the batch
     if (nmax - j <= HHR_NT) LAUNCH(hh_panel_reg_kernel<1>, ntasks, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);

@@ -508,6 +508,7 @@ struct TriRootReq {
 };
 constexpr int HH_SMEM_ROWS = 768;   // = HHS_ROWS of hh_panel_smem_kernel
 constexpr int HH_REG_ROWS = 512;    // = 256 threads x 2 rows of hh_panel_reg_kernel<2>
+constexpr int HH_REGCL_ROWS = 4096; // = 8 CTAs x 256 threads x 2 rows of hh_panel_reg_cluster_kernel<2>
 template <class Pool>
 inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work, Uploader& up, cudaStream_t s,
                              FlopCounter* fc = nullptr, int tsqr_m = -1) {
@@ -568,9 +569,13 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   const size_t nsm = sorted_reqs.size() - nrg;
   for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && (q.n < 512 || many)) sorted_reqs.push_back(q);
   const size_t nsmall = sorted_reqs.size() - nrg - nsm;
-  int nmax_mid = 0;
-  for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && !many && q.n >= 512 && q.n <= SM_ROWS) { sorted_reqs.push_back(q); nmax_mid = std::max(nmax_mid, q.n); }
-  const size_t nmid = sorted_reqs.size() - nrg - nsm - nsmall;
+  int nmax_rc = 0, nmax_mid = 0;
+  static const bool no_regcl = getenv("AIFMM_NO_REGCLUSTER") != nullptr;   // debug toggle
+  const int RC_ROWS = no_regcl ? 0 : HH_REGCL_ROWS;
+  for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && !many && q.n <= RC_ROWS) { sorted_reqs.push_back(q); nmax_rc = std::max(nmax_rc, q.n); }
+  const size_t nrc = sorted_reqs.size() - nrg - nsm - nsmall;
+  for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && !many && q.n > RC_ROWS && q.n <= SM_ROWS) { sorted_reqs.push_back(q); nmax_mid = std::max(nmax_mid, q.n); }
+  const size_t nmid = sorted_reqs.size() - nrg - nsm - nsmall - nrc;
   for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && !many && q.n > SM_ROWS) sorted_reqs.push_back(q);
   const std::vector<TriRootReq>& R = sorted_reqs;
   std::vector<char> tb(tsz * reqs.size());
@@ -596,12 +601,13 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   for (int j = 0; j < rmax; j += HH_PANEL) {
     if (g_prof.on) g_prof.begin(s);
     const char* d0 = static_cast<const char*>(dt);
-    const size_t o1 = nrg, o2 = o1 + nsm, o3 = o2 + nsmall, o4 = o3 + nmid;
+    const size_t o1 = nrg, o2 = o1 + nsm, o3 = o2 + nsmall, o4 = o3 + nrc, o5 = o4 + nmid;
     if (nrg && j < nmax_rg) launch_hh_panel(d0, (int)nrg, j, s, 4, nmax_rg);
     if (nsm && j < nmax_sm) launch_hh_panel(d0 + o1 * tsz, (int)nsm, j, s, 3, nmax_sm);
     if (nsmall) launch_hh_panel(d0 + o2 * tsz, (int)nsmall, j, s, 0, 0);
-    if (nmid) launch_hh_panel(d0 + o3 * tsz, (int)nmid, j, s, 2, nmax_mid);
-    if (reqs.size() > o4) launch_hh_panel(d0 + o4 * tsz, (int)(reqs.size() - o4), j, s, 1, 0);
+    if (nrc) launch_hh_panel(d0 + o3 * tsz, (int)nrc, j, s, 5, nmax_rc);
+    if (nmid) launch_hh_panel(d0 + o4 * tsz, (int)nmid, j, s, 2, nmax_mid);
+    if (reqs.size() > o5) launch_hh_panel(d0 + o5 * tsz, (int)(reqs.size() - o5), j, s, 1, 0);
     // fused trailing update: one CTA per (task, 64-column block of the trailing matrix)
     std::vector<int2> ut;
     for (size_t i = 0; i < reqs.size(); ++i) {
