@@ -541,6 +541,8 @@ gj_panel_cluster_kernel(const GJBTask* __restrict__ tasks, int j, int cap_rows) 
   __shared__ double red[32];
   __shared__ int redi[32];
   __shared__ double prow[GJB];
+  __shared__ double s_gm;
+  __shared__ int s_gp;
   __shared__ double Li[GJB][GJB + 1], Ui[GJB][GJB + 1];
   __shared__ int pv[GJB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -566,15 +568,32 @@ gj_panel_cluster_kernel(const GJBTask* __restrict__ tasks, int j, int cap_rows) 
     if (c >= lo && c < hi)
       for (int cc = tid; cc < nbw; cc += GJ_NT) sh.rowc[ph][cc] = P[(c - lo) * LP + cc];
     cl.sync();
-    // global pivot
-    double gm = -1.0;
-    int gp = 0x7fffffff, go = 0;
-    for (int q = 0; q < GJC; ++q) {
-      const GjcShared* o = cl.map_shared_rank(&sh, q);
-      const double ov = o->v[ph];
-      const int oi = o->idx[ph];
-      if (ov > gm || (ov == gm && oi < gp)) { gm = ov; gp = oi; go = q; }
+    // global pivot: lanes 0..GJC-1 of warp 0 read the CTAs' candidates in parallel (one round
+    // of DSMEM loads), a shuffle argmax picks (largest, lowest row), warp 0 fetches the pivot row
+    if (warp == 0) {
+      double ov = -1.0;
+      int oi = 0x7fffffff;
+      if (lane < GJC) {
+        const GjcShared* o = cl.map_shared_rank(&sh, lane);
+        ov = o->v[ph];
+        oi = o->idx[ph];
+      }
+      int oq = lane;
+      for (int off = 4; off > 0; off >>= 1) {   // GJC = 8 lanes
+        const double v2 = __shfl_xor_sync(0xffffffffu, ov, off);
+        const int i2 = __shfl_xor_sync(0xffffffffu, oi, off);
+        const int q2 = __shfl_xor_sync(0xffffffffu, oq, off);
+        if (v2 > ov || (v2 == ov && i2 < oi)) { ov = v2; oi = i2; oq = q2; }
+      }
+      ov = __shfl_sync(0xffffffffu, ov, 0);
+      oi = __shfl_sync(0xffffffffu, oi, 0);
+      oq = __shfl_sync(0xffffffffu, oq, 0);
+      if (lane == 0) { s_gm = ov; s_gp = oi; }
+      if (ov > 0.0 && lane < nbw) prow[lane] = cl.map_shared_rank(&sh, oq)->cand[ph][lane];
     }
+    __syncthreads();
+    const double gm = s_gm;
+    const int gp = s_gp;
     if (!(gm > 0.0)) {
       if (rank == 0 && tid == 0) *tk.info = j + c + 1;
       cl.sync();
@@ -582,9 +601,7 @@ gj_panel_cluster_kernel(const GJBTask* __restrict__ tasks, int j, int cap_rows) 
     }
     const int oc = min(GJC - 1, c / chunk);   // owner of row c
     if (rank == 0 && tid == 0) tk.piv[j + c] = j + gp;
-    // pivot row (old row gp) for everyone; the owner of gp receives old row c
-    const GjcShared* wo = cl.map_shared_rank(&sh, go);
-    for (int cc = tid; cc < nbw; cc += GJ_NT) prow[cc] = wo->cand[ph][cc];
+    // the owner of the pivot row receives old row c
     if (gp != c && gp >= lo && gp < hi) {
       const GjcShared* co = cl.map_shared_rank(&sh, oc);
       for (int cc = tid; cc < nbw; cc += GJ_NT) P[(gp - lo) * LP + cc] = co->rowc[ph][cc];
@@ -920,6 +937,8 @@ pqr_cluster_kernel(const PqrTask* __restrict__ tasks, int smem_cap) {
   __shared__ int redi[32];
   __shared__ double s_part, s_max;
   __shared__ int s_idx;
+  __shared__ double s_bc[3];
+  __shared__ int s_bci;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = PQR_NT / 32;
   const double tau = tk.tol * (tk.fnorm ? *tk.fnorm : 1.0);
@@ -945,11 +964,18 @@ pqr_cluster_kernel(const PqrTask* __restrict__ tasks, int smem_cap) {
     block_sum_max<PQR_NT>(part, v, red, &part, &v);
     if (tid == 0) { s_part = part; s_max = v; }
     cl.sync();
-    double res2 = 0.0, mx = -1.0;
-    for (int q = 0; q < PQC; ++q) {
-      res2 += *cl.map_shared_rank(&s_part, q);
-      mx = fmax(mx, *cl.map_shared_rank(&s_max, q));
+    // warp 0 fetches the PQC partials in one parallel round of DSMEM loads
+    if (warp == 0) {
+      double a2 = 0.0, b2 = -1.0;
+      if (lane < PQC) { a2 = *cl.map_shared_rank(&s_part, lane); b2 = *cl.map_shared_rank(&s_max, lane); }
+      for (int o = 4; o > 0; o >>= 1) {
+        a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+        b2 = fmax(b2, __shfl_xor_sync(0xffffffffu, b2, o));
+      }
+      if (lane == 0) { s_bc[0] = a2; s_bc[1] = b2; }
     }
+    __syncthreads();
+    const double res2 = s_bc[0], mx = s_bc[1];
     const bool ok = !(sqrt(res2) > tau);
     if (ok && t_trunc < 0) t_trunc = t;
     if ((t >= tk.tmin && ok) || t >= tk.tmax) break;
@@ -961,8 +987,13 @@ pqr_cluster_kernel(const PqrTask* __restrict__ tasks, int smem_cap) {
     cand = block_min_int<PQR_NT>(cand, redi);
     if (tid == 0) s_idx = cand;
     cl.sync();
-    int j = 0x7fffffff;
-    for (int q = 0; q < PQC; ++q) j = min(j, *cl.map_shared_rank(&s_idx, q));
+    if (warp == 0) {
+      int jj = (lane < PQC) ? *cl.map_shared_rank(&s_idx, lane) : 0x7fffffff;
+      for (int o = 4; o > 0; o >>= 1) jj = min(jj, __shfl_xor_sync(0xffffffffu, jj, o));
+      if (lane == 0) s_bci = jj;
+    }
+    __syncthreads();
+    const int j = s_bci;
     const int jo = min(PQC - 1, j / cw);       // owner rank of column j
     // fetch column j (owner's slice) into w
     {
@@ -1002,8 +1033,13 @@ pqr_cluster_kernel(const PqrTask* __restrict__ tasks, int smem_cap) {
       p2 = block_sum<PQR_NT>(p2, red);
       if (tid == 0) s_part = p2;
       cl.sync();
-      double n2 = 0.0;
-      for (int q = 0; q < PQC; ++q) n2 += *cl.map_shared_rank(&s_part, q);
+      if (warp == 0) {
+        double a2 = (lane < PQC) ? *cl.map_shared_rank(&s_part, lane) : 0.0;
+        for (int o = 4; o > 0; o >>= 1) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+        if (lane == 0) s_bc[2] = a2;
+      }
+      __syncthreads();
+      const double n2 = s_bc[2];
       // gather the full w from the row owners
       for (int r = tid; r < m; r += PQR_NT) {
         const int own = min(PQC - 1, r / max(rw, 1));

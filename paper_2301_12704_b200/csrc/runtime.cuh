@@ -567,12 +567,14 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   const size_t nrg = sorted_reqs.size();
   for (const auto& q : reqs) if (q.n > HH_REG_ROWS && q.n <= HH_SMEM_ROWS) { sorted_reqs.push_back(q); nmax_sm = std::max(nmax_sm, q.n); }
   const size_t nsm = sorted_reqs.size() - nrg;
-  for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && (q.n < 512 || many)) sorted_reqs.push_back(q);
+  static const bool no_regcl = getenv("AIFMM_NO_REGCLUSTER") != nullptr;   // debug toggle
+  static const bool regcl_many = getenv("AIFMM_REGCL_FEW") == nullptr;     // debug toggle
+  const int RC_ROWS = no_regcl ? 0 : HH_REGCL_ROWS;
+  auto to_rc = [&](const TriRootReq& q) { return q.n > HH_SMEM_ROWS && q.n <= RC_ROWS && (!many || regcl_many); };
+  for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && (q.n < 512 || many) && !to_rc(q)) sorted_reqs.push_back(q);
   const size_t nsmall = sorted_reqs.size() - nrg - nsm;
   int nmax_rc = 0, nmax_mid = 0;
-  static const bool no_regcl = getenv("AIFMM_NO_REGCLUSTER") != nullptr;   // debug toggle
-  const int RC_ROWS = no_regcl ? 0 : HH_REGCL_ROWS;
-  for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && !many && q.n <= RC_ROWS) { sorted_reqs.push_back(q); nmax_rc = std::max(nmax_rc, q.n); }
+  for (const auto& q : reqs) if (to_rc(q)) { sorted_reqs.push_back(q); nmax_rc = std::max(nmax_rc, q.n); }
   const size_t nrc = sorted_reqs.size() - nrg - nsm - nsmall;
   for (const auto& q : reqs) if (q.n > HH_SMEM_ROWS && !many && q.n > RC_ROWS && q.n <= SM_ROWS) { sorted_reqs.push_back(q); nmax_mid = std::max(nmax_mid, q.n); }
   const size_t nmid = sorted_reqs.size() - nrg - nsm - nsmall - nrc;

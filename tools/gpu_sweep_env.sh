@@ -1,5 +1,7 @@
 #!/bin/bash
-# factor time + residual of config 2 under debug toggles of the compression stage
-for env in "X=1" "AIFMM_NO_TSQR=1" "AIFMM_TSQR_MMAX=64" "AIFMM_TSQR_MMAX=100000" "AIFMM_HH_CLUSTER=1"; do
-  echo "$env $(env $env timeout 600 python tools/gpu_perf.py 1 2>/dev/null | grep -E '^\{|residual' | tail -2 | cut -c1-110 | tr '\n' ' ')"
+# factor time of configs 2 and 3 under routing toggles
+for env in "X=1" "AIFMM_REGCL_FEW=1"; do
+  for cfg in 1 2; do
+    echo "$env cfg$cfg $(env $env timeout 600 python tools/gpu_perf.py $cfg 2>/dev/null | grep '^{' | tail -1 | cut -c1-150)"
+  done
 done

@@ -10,6 +10,9 @@ rounded, each compared with the reference run:
     level-start orthonormalisation, R13) applied to the row-reversed matrix -- the same R (up to
     row signs) and the same Q up to the permutation, rounded along another reflector sequence;
   * both at once;
+  * the compression threshold tol_c * ||F||_F (R8) scaled by (1 +- 1e-12) and (1 +- 1e-9): a
+    truncation decision that sits within rounding distance of the threshold flips, as it does
+    under any change of reduction order;
   * exact-arithmetic-equivalent choices of the kind a GPU implementation makes: CholeskyQR2 for
     the level-start orthonormalisation, a TSQR R factor (row chunks of <= 512 rows, R of the
     stacked chunk R's) for the first RRQR stage, Gauss-Jordan with partial pivoting for the
@@ -86,11 +89,11 @@ def inv_gauss_jordan(P):
     return A[:, n:]
 
 
-def run(cfg, pts, b, inv=None, qr=None):
+def run(cfg, pts, b, inv=None, qr=None, tol_c=None):
     np.linalg.inv = inv or _inv
     np.linalg.qr = qr or _qr
     try:
-        o = F.AIFMM(pts, cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol).factor()
+        o = F.AIFMM(pts, cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol, tol_c=tol_c).factor()
         return o, o.solve(b)
     finally:
         np.linalg.inv, np.linalg.qr = _inv, _qr
@@ -104,7 +107,11 @@ def main():
     out = {"workload": cfg.name, "tol": cfg.tol, "rel_solution_diff": {}, "final_rank_mismatches_per_level": {}}
     for name, kw in (("lu_solve", {"inv": inv_lu}), ("qr_reversed_rows", {"qr": qr_reversed}),
                      ("lu_solve+qr_reversed_rows", {"inv": inv_lu, "qr": qr_reversed}),
-                     ("gpu_like_choices", {"inv": inv_gauss_jordan, "qr": qr_gpu_like})):
+                     ("gpu_like_choices", {"inv": inv_gauss_jordan, "qr": qr_gpu_like}),
+                     ("tol_c*(1+1e-12)", {"tol_c": cfg.tol * (1 + 1e-12)}),
+                     ("tol_c*(1-1e-12)", {"tol_c": cfg.tol * (1 - 1e-12)}),
+                     ("tol_c*(1+1e-9)", {"tol_c": cfg.tol * (1 + 1e-9)}),
+                     ("tol_c*(1-1e-9)", {"tol_c": cfg.tol * (1 - 1e-9)})):
         o2, x2 = run(cfg, pts, b, **kw)
         out["rel_solution_diff"][name] = float(np.linalg.norm(x2 - x1) / np.linalg.norm(x1))
         out["final_rank_mismatches_per_level"][name] = {
