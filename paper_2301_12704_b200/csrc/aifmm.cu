@@ -13,6 +13,7 @@
 //   solve  : Algorithm 4 replaying the records on nrhs columns.
 #include <nvtx3/nvToolsExt.h>
 #include <chrono>
+#include <functional>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1122,7 +1123,11 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
 }
 
 // Alg. 3 lines P:1118-1129 for the pending pairs S (colour-batched, R12; R14, R15)
-static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& S) {
+// after_ranks runs as soon as the new ranks are known (before the regrow / redirection
+// planning): the caller launches the colour's pivot inverses there, which need only the final
+// bases, so the GPU works on them while the host plans the redirection.
+static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& S,
+                     const std::function<void()>& after_ranks) {
   std::map<int, std::vector<int>> part;
   for (auto& pr : S) {
     part[pr.first].push_back(pr.second);
@@ -1134,7 +1139,10 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
     if (!f.E[kv.first]) aff.push_back(kv.first);
   }
   const int na = (int)aff.size();
-  if (!na) return;
+  if (!na) {
+    after_ranks();
+    return;
+  }
   if (g_prof.on) g_prof.begin(c.s);
   // phase 1 in groups whose temporaries stay under a workspace budget
   std::vector<int> tgt(na, 0);
@@ -1168,6 +1176,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
     if (f.k[b] > f.kcap[b]) grown.push_back(b);
     c.stats[AIFMM_STAT_COMPRESSIONS] += 1;
   }
+  after_ranks();
   regrow(c, f, grown);
   for (int b : aff) {   // only the compressed boxes' ranks changed
     int ni;
@@ -1234,6 +1243,7 @@ struct SchurPlan {
   std::vector<std::vector<std::pair<int, int>>> wcol;   // (q, column offset in W_i)
   std::vector<int> tot;
   std::vector<std::pair<int, int>> new_pending;
+  std::vector<double*> W;   // W_i = G[:, 0:m] R_i (eliminate_invert -> eliminate_update)
 };
 static int wcol_of(const std::vector<std::pair<int, int>>& w, int q) {
   for (auto& e : w)
@@ -1306,8 +1316,12 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
   g_prof.hlap("tg.tasks");
 }
 
-static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
+// Steps 1-2 of a colour's elimination: pivot inverses and W_i = G[:, 0:m] R_i.  They need only
+// the colour's final bases and near blocks (no far M2L block), so they are launched before the
+// redirection of the colour's compression is planned.
+static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
   const int l = f.l;
+  (void)l;
   if (g_prof.on) g_prof.begin(c.s);
   // 1. assemble P_i = [[K_ii, U_i],[V_i^T, 0]] into G_i and invert in place (R16)
   CopyBatch cb;
@@ -1363,7 +1377,15 @@ static void eliminate_colour(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     }
   }
   g.run(c.up, c.s, &c.fc_all);
-  if (g_prof.on) { g_prof.end("elim.W"); g_prof.begin(c.s); }
+  P.W = std::move(W);
+  if (g_prof.on) g_prof.end("elim.W");
+}
+
+static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
+  const int l = f.l;
+  const std::vector<double*>& W = P.W;
+  CopyBatch cb;
+  if (g_prof.on) g_prof.begin(c.s);
   // 3. Schur updates (planned) are launched first; the new blocks (p,i) = C G12,
   //    (i,q) = G21 R = W_z, (i,i) = -G22 (R17) are planned while they run (they touch no
   //    Schur target: (p,i) with i in the colour is never a target of the colour, whose boxes
@@ -1488,10 +1510,11 @@ static void factor_levels(Ctx& c) {
       SchurPlan plan;
       plan_schur(c, f, cs, plan);   // host work, overlaps the previous colour's kernels
       g_prof.begin(c.s);
-      if (!S.empty()) compress(c, f, S);
+      if (!S.empty()) compress(c, f, S, [&] { eliminate_invert(c, f, cs, plan); });
+      else eliminate_invert(c, f, cs, plan);
       g_prof.end(("compress.L" + std::to_string(l)).c_str());
       g_prof.begin(c.s);
-      eliminate_colour(c, f, cs, plan);
+      eliminate_update(c, f, cs, plan);
       g_prof.end(("eliminate.L" + std::to_string(l)).c_str());
     }
     AIFMM_REQUIRE(f.pending.empty(), AIFMM_ESINGULAR_PIVOT, "pending far fill-ins at level end");
