@@ -254,7 +254,10 @@ static Ctx& ctx() {
     AIFMM_CUDA(cudaStreamCreateWithFlags(&g_ctx->s, cudaStreamNonBlocking));
     g_ctx->own_stream = true;
     g_ctx->up.init(g_ctx->s);
-    g_before_launch = [] { if (g_ctx) g_ctx->up.flush(); };
+    g_before_launch = [] {
+      g_expose.launching();
+      if (g_ctx) g_ctx->up.flush();
+    };
     AIFMM_CUDA(cudaMalloc(&g_ctx->dflag, 64));
   }
   return *g_ctx;
@@ -557,6 +560,7 @@ static void build_nnca(Ctx& c) { build_nnca(c, c.nn, c.tol / 100.0, c.persist); 
 static inline int live(const FLevel& f, int b) { return f.E[b] ? f.k[b] : f.m[b]; }
 
 static void setup_level(Ctx& c, int l) {
+  g_expose.set("setup");
   g_prof.hstart();
   FLevel& f = c.fl[l];
   const int d = c.d, nb = 1 << (d * l);
@@ -681,7 +685,7 @@ static void setup_level(Ctx& c, int l) {
         const int q = nbl[t];
         const Blk& blk = f.nearb.at_slot(b, t);
         if (l == c.L) {
-          kt.push_back(KEvalTask{blk.p, blk.ld, m, f.m[q], nullptr, nullptr, (int)c.off[l][b], (int)c.off[l][q]});
+          // evaluated from the block table below (keval_table_kernel, mode 1)
         } else {
           for (int ch = 0; ch < (1 << d); ++ch) {
             int c1 = (b << d) | ch;
@@ -697,15 +701,7 @@ static void setup_level(Ctx& c, int l) {
           }
         }
       }
-      // M2L A(sk b, sk q)
-      int ni;
-      const int* il = c.ilist(l, b, &ni);
-      for (int t = 0; t < ni; ++t) {
-        const int q = il[t];
-        const Blk& a = f.A.at_slot(b, t);
-        if (f.k[b] && f.k[q])
-          kt.push_back(KEvalTask{a.p, a.ld, f.k[b], f.k[q], nl.dsk + nl.skoff[b], nl.dsk + nl.skoff[q], 0, 0});
-      }
+      // M2L A(sk b, sk q): evaluated from the block table below (mode 0)
     }
   });
   g_prof.hlap("setup.par");
@@ -718,6 +714,23 @@ static void setup_level(Ctx& c, int l) {
   g_prof.hlap("setup.plan");
   cb.run(c.up, c.s);
   if (!kt.empty()) launch_keval(c.up.put(kt), (int)kt.size(), 4, c.pts, c.kp, c.dflag, c.s);
+  {
+    // kernel-entry blocks straight from the block tables: M2L A(sk b, sk q) at every
+    // level, the near blocks at the leaf level (one upload of the tables, no task lists)
+    static_assert(sizeof(Blk) == sizeof(BlkDev), "Blk / BlkDev layout");
+    const void* dA = c.up.put(f.A.v);
+    const int* dicnt = c.up.put(c.icnt[l]);
+    const int* diidx = c.up.put(c.iidx[l]);
+    const long long* dsko = c.up.put(nl.skoff);
+    launch_keval_table(dA, dicnt, diidx, nb, c.icap, 0, nl.dsk, dsko, c.pts, c.kp, c.dflag, c.s);
+    if (l == c.L) {
+      const void* dN = c.up.put(f.nearb.v);
+      const int* dncnt = c.up.put(c.ncnt[l]);
+      const int* dnidx = c.up.put(c.nidx[l]);
+      const long long* doff = c.up.put(c.off[l]);
+      launch_keval_table(dN, dncnt, dnidx, nb, c.ncap, 1, nullptr, doff, c.pts, c.kp, c.dflag, c.s);
+    }
+  }
   g_prof.hlap("setup.launch");
   // level l+1's per-level state is dead once copied: mark its pool free (reused by level l-1,
   // or given back by an out-of-memory trim)
@@ -824,6 +837,7 @@ static void bases_pqr(Ctx& c, FLevel& f, std::vector<double*>& T, std::vector<do
 }
 
 static void orthonormalise(Ctx& c, FLevel& f) {
+  g_expose.set("orth");
   const int l = f.l;
   std::vector<double*> T(f.nb, nullptr), T2(f.nb, nullptr);
   g_prof.begin(c.s);
@@ -934,6 +948,7 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
   AIFMM_CUDA(cudaMemsetAsync(dt, 0, sizeof(int) * 4 * na, c.s));
   std::vector<char> full(na, 0);
   // symmetric (R27): only the U side is compressed; V_b's new columns are copies of U_b's
+  g_expose.set("cmp.gather");
   const bool sym = c.symmetric;
   g_prof.hstart();
   for (int a = 0; a < na; ++a) {
@@ -974,6 +989,7 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
   launch_norm(c.up.put(nt), (int)nt.size(), c.s);
   if (g_prof.on) { g_prof.end("cmp.gather"); g_prof.begin(c.s); }
   // projection W <- (I - B B^T) W, i.e. WT <- WT - (WT B) B^T
+  g_expose.set("cmp.proj");
   GemmBatch g;
   std::vector<double*> tu(na), tv(na);
   for (int a = 0; a < na; ++a) {
@@ -1009,7 +1025,9 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     tr.push_back(TriRootReq{su[a].WT, nu, nu, m, su[a].M, m});
     if (!sym) tr.push_back(TriRootReq{sv[a].WT, nu, nu, m, sv[a].M, m});
   }
+  g_expose.set("cmp.tri");
   batched_tri_root(tr, c.work, c.up, c.s, &c.fc_all);
+  g_expose.set("cmp.pqr");
   if (g_prof.on) { g_prof.end("cmp.proj+triroot"); g_prof.begin(c.s); }
   struct SideW { double* W; int nc; };
   std::vector<SideW> wu(na), wv(na);
@@ -1031,6 +1049,7 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
   }
   if (!pq.empty()) run_pqr(pq, c.up, c.s);
   std::vector<int> th = d2h(c, dt, 4 * na);
+  g_expose.set("cmp.post");
   if (g_prof.on) { g_prof.end("cmp.pqrA"); g_prof.begin(c.s); }
   tgt.assign(na, 0);
   if (sym) {
@@ -1128,6 +1147,7 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
 // bases, so the GPU works on them while the host plans the redirection.
 static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& S,
                      const std::function<void()>& after_ranks) {
+  g_expose.set("cmp.pre");
   std::map<int, std::vector<int>> part;
   for (auto& pr : S) {
     part[pr.first].push_back(pr.second);
@@ -1177,6 +1197,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
     c.stats[AIFMM_STAT_COMPRESSIONS] += 1;
   }
   after_ranks();
+  g_expose.set("cmp.redirect");
   regrow(c, f, grown);
   for (int b : aff) {   // only the compressed boxes' ranks changed
     int ni;
@@ -1251,6 +1272,7 @@ static int wcol_of(const std::vector<std::pair<int, int>>& w, int q) {
   return -1;
 }
 static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
+  g_expose.set("plan");
   const int l = f.l;
   g_prof.hstart();
   P.nbs.assign(cs.size(), {});
@@ -1320,6 +1342,7 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
 // the colour's final bases and near blocks (no far M2L block), so they are launched before the
 // redirection of the colour's compression is planned.
 static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
+  g_expose.set("elim.inv");
   const int l = f.l;
   (void)l;
   if (g_prof.on) g_prof.begin(c.s);
@@ -1382,6 +1405,7 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
 }
 
 static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
+  g_expose.set("elim.upd");
   const int l = f.l;
   const std::vector<double*>& W = P.W;
   CopyBatch cb;
@@ -1475,6 +1499,7 @@ static void deferred_checks(Ctx& c) {
 
 static void factor_levels(Ctx& c);
 static void factor_all(Ctx& c) {
+  g_expose.set("factor.start");
   c.fl.assign(c.L + 1, FLevel{});
   AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
   try {
@@ -1538,6 +1563,7 @@ static void factor_levels(Ctx& c) {
     f.Xtot = f.xrow[f.nb];
     f.Ztot = f.zrow[f.nb];
   }
+  g_expose.set("top");
   // top: M = (Z_p, y_q) over level-2 boxes; inverted in place (R19 dense GJ)
   g_prof.begin(c.s);
   FLevel& f = c.fl[2];
@@ -1568,6 +1594,8 @@ static void factor_levels(Ctx& c) {
   c.work.reset();
   g_prof.end("top");
   g_prof.dump("factor");
+  g_expose.set("after");
+  g_expose.dump();
 }
 
 // ------------------------------------------------------------------------------------ solve

@@ -1,5 +1,6 @@
 // common.cuh — shared device/host utilities of libaifmm (B200, sm_100a).
 #pragma once
+#include <unordered_map>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
@@ -51,10 +52,18 @@ extern void (*g_before_launch)();
 // (the default allowance is 48 KB minus the kernel's static shared memory).
 template <class F>
 inline void ensure_dyn_smem(F* func, size_t bytes) {
+  // the allowance already granted per kernel is cached (no driver query per launch)
+  static thread_local std::unordered_map<const void*, int> granted;
+  auto it = granted.find(reinterpret_cast<const void*>(func));
+  if (it != granted.end() && (int)bytes <= it->second) return;
   cudaFuncAttributes fa{};
   AIFMM_CUDA(cudaFuncGetAttributes(&fa, func));
-  if ((int)bytes > fa.maxDynamicSharedSizeBytes)
+  int have = fa.maxDynamicSharedSizeBytes;
+  if ((int)bytes > have) {
     AIFMM_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = (int)bytes;
+  }
+  granted[reinterpret_cast<const void*>(func)] = have;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -101,6 +110,12 @@ struct GJTask {
 
 // Kernel-entry block: out[i,j] = K(x_{rows[i]}, x_{cols[j]}) (diag value when equal).
 // rows/cols == nullptr means the contiguous range row0 + i / col0 + j.
+// Device view of the host planner's per-level block table entry (aifmm.cu Blk: same layout).
+struct BlkDev {
+  double* p;
+  int ld, rows, cols;
+};
+
 struct KEvalTask {
   double* out;
   int ld, nr, nc;

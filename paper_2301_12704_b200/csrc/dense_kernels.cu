@@ -1925,6 +1925,38 @@ __global__ void keval_tasks_kernel(const KEvalTask* __restrict__ tasks, const do
   }
 }
 
+// Kernel-entry blocks straight from a level's block table (no per-block task list): CTA s
+// handles slot s = b * cap + t of box b's list (N(b) or IL(b), entry q = idx[s]):
+//   mode 0 (M2L): A(sk_b, sk_q) with the skeleton index lists sk + skoff[.];
+//   mode 1 (leaf near blocks): A(points(b), points(q)) with point ranges off[.].
+// The block sizes are the table entry's rows / cols; empty slots and empty blocks exit.
+__global__ void keval_table_kernel(const BlkDev* __restrict__ v, const int* __restrict__ cnt,
+                                   const int* __restrict__ idx, int cap, int mode,
+                                   const int* __restrict__ sk, const long long* __restrict__ base,
+                                   const double* __restrict__ pts, KernelParams kp, int* __restrict__ flag) {
+  const long long slot = blockIdx.x;
+  const int b = (int)(slot / cap), t = (int)(slot % cap);
+  if (t >= cnt[b]) return;
+  const BlkDev blk = v[slot];
+  const int nr = blk.rows, nc = blk.cols;
+  if (nr <= 0 || nc <= 0 || blk.p == nullptr) return;
+  const int q = idx[slot];
+  const long long rb = base[b], cb = base[q];
+  for (int e = threadIdx.x; e < nr * nc; e += blockDim.x) {
+    const int i = e % nr, j = e / nr;
+    const int gi = mode == 0 ? sk[rb + i] : (int)(rb + i);
+    const int gj = mode == 0 ? sk[cb + j] : (int)(cb + j);
+    const double val = kernel_entry(kp, pts, gi, gj);
+    if (!isfinite(val)) *flag = 1;
+    blk.p[(size_t)j * blk.ld + i] = val;
+  }
+}
+
+void launch_keval_table(const void* v, const int* cnt, const int* idx, int nb, int cap, int mode, const int* sk,
+                        const long long* base, const double* pts, KernelParams kp, int* flag, cudaStream_t s) {
+  LAUNCH(keval_table_kernel, nb * cap, 128, 0, s, static_cast<const BlkDev*>(v), cnt, idx, cap, mode, sk, base, pts, kp, flag);
+}
+
 // ------------------------------------------------------------------------------ copies, norms
 __global__ void copy_tasks_kernel(const CopyTask* __restrict__ tasks) {
   const CopyTask tk = tasks[blockIdx.x];

@@ -1,5 +1,6 @@
 // runtime.cuh — host-side runtime pieces of libaifmm: device pools, task upload arena, batch builders.
 #pragma once
+#include <exception>
 #include <thread>
 #include <algorithm>
 #include <chrono>
@@ -22,6 +23,8 @@ void launch_gj(const GJTask* t, int ntasks, int nmax, int mode, cudaStream_t s);
 void launch_pqr(const PqrTask* t, int ntasks, size_t smem_doubles, cudaStream_t s);
 void launch_pqr_cluster(const PqrTask* t, int ntasks, cudaStream_t s);
 void launch_keval(const KEvalTask* t, int ntasks, int ysplit, const double* pts, KernelParams kp, int* flag, cudaStream_t s);
+void launch_keval_table(const void* v, const int* cnt, const int* idx, int nb, int cap, int mode, const int* sk,
+                        const long long* base, const double* pts, KernelParams kp, int* flag, cudaStream_t s);
 void launch_copy(const CopyTask* t, int ntasks, int ysplit, cudaStream_t s);
 void launch_norm(const NormTask* t, int ntasks, cudaStream_t s);
 void launch_chol_inv(const CholTask* t, int ntasks, int kmax, cudaStream_t s);
@@ -81,6 +84,53 @@ struct Prof {
   }
 };
 inline Prof g_prof;
+
+// Exposed host time (AIFMM_EXPOSE=1): wall time from a stream synchronisation returning to the
+// next kernel launch -- the GPU is idle for all of it -- accumulated under the current phase.
+struct Exposure {
+  bool on = getenv("AIFMM_EXPOSE") != nullptr;
+  const char* phase = "?";
+  bool pending = false;
+  std::chrono::steady_clock::time_point t;
+  std::map<std::string, std::pair<double, int>> ms;
+  std::map<std::string, double> wall;   // host wall time per phase (incl. waits)
+  double wait_ms = 0.0;                 // host blocked in stream synchronisations
+  std::chrono::steady_clock::time_point tw, tph;
+  void set(const char* p) {
+    if (!on) { phase = p; return; }
+    auto n = std::chrono::steady_clock::now();
+    wall[phase] += std::chrono::duration<double, std::milli>(n - tph).count();
+    tph = n;
+    phase = p;
+  }
+  void wait_begin() { if (on) tw = std::chrono::steady_clock::now(); }
+  void synced() {
+    if (on) {
+      pending = true;
+      t = std::chrono::steady_clock::now();
+      wait_ms += std::chrono::duration<double, std::milli>(t - tw).count();
+    }
+  }
+  void launching() {
+    if (!on || !pending) return;
+    auto& e = ms[phase];
+    e.first += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+    e.second += 1;
+    pending = false;
+  }
+  void dump() {
+    if (!on) return;
+    fprintf(stderr, "[aifmm exposed host ms]");
+    for (auto& kv : ms) fprintf(stderr, " %s=%.2f(%d)", kv.first.c_str(), kv.second.first, kv.second.second);
+    fprintf(stderr, " | sync wait %.2f | wall:", wait_ms);
+    for (auto& kv : wall) fprintf(stderr, " %s=%.2f", kv.first.c_str(), kv.second);
+    fprintf(stderr, "\n");
+    ms.clear();
+    wall.clear();
+    wait_ms = 0.0;
+  }
+};
+inline Exposure g_expose;
 
 // ---------------------------------------------------------------------------------- pools
 // Device memory: one process-wide cache of fixed-size chunks (oversize requests get a
@@ -245,9 +295,11 @@ class Uploader {
   }
   void sync() {
     flush();
+    g_expose.wait_begin();
     AIFMM_CUDA(cudaStreamSynchronize(s_));
     used_ = flushed_ = 0;
     ++syncs;
+    g_expose.synced();
   }
   long long syncs = 0;
 
@@ -293,6 +345,16 @@ class GemmBatch {
   bool empty() const { return tasks_.empty(); }
   size_t size() const { return tasks_.size(); }
   size_t nterms() const { return terms_.size(); }
+  // o's tasks after this batch's (term indices shifted; order preserved)
+  void append(const GemmBatch& o) {
+    const int off = (int)terms_.size();
+    for (GemmTask t : o.tasks_) {
+      t.term_begin += off;
+      t.term_end += off;
+      tasks_.push_back(t);
+    }
+    terms_.insert(terms_.end(), o.terms_.begin(), o.terms_.end());
+  }
   GemmTerm& term_ref(size_t i) { return terms_[i]; }
   // Deterministic split-K: single-term tasks with a long K and few output tiles are split into
   // S partial GEMMs into workspace slices, then reduced in a fixed order by a second launch.
@@ -397,8 +459,18 @@ inline int parallel_chunks(int n, int min_per_thread, F&& fn) {
     return 1;
   }
   std::vector<std::thread> th;
-  for (int t = 0; t < T; ++t) th.emplace_back([&, t] { fn((int)((long long)n * t / T), (int)((long long)n * (t + 1) / T), t); });
+  std::vector<std::exception_ptr> err(T);
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      try {
+        fn((int)((long long)n * t / T), (int)((long long)n * (t + 1) / T), t);
+      } catch (...) {
+        err[t] = std::current_exception();
+      }
+    });
   for (auto& x : th) x.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);   // the first failing chunk's error, on the calling thread
   return T;
 }
 
