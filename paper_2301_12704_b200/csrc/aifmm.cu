@@ -869,6 +869,7 @@ static void orthonormalise(Ctx& c, FLevel& f) {
     for (int t = 0; t < ni; ++t) {
       int q = il[t];
       if (!f.k[q]) continue;
+      if (k <= ORTH_SW_KMAX && f.k[q] <= ORTH_SW_KMAX) continue;   // orth_sandwich_kernel below
       double* tp = c.work.d((size_t)k * f.k[q]);
       tmpA[(size_t)b * c.icap + t] = tp;
       const Blk& a = f.A.at_slot(b, t);
@@ -892,12 +893,20 @@ static void orthonormalise(Ctx& c, FLevel& f) {
     for (int t = 0; t < ni; ++t) {
       int q = il[t];
       if (!f.k[q]) continue;
+      if (k <= ORTH_SW_KMAX && f.k[q] <= ORTH_SW_KMAX) continue;
       const Blk& a = f.A.at_slot(b, t);
       g.task(a.p, a.ld, k, f.k[q], 0.0);
       g.term(1.0, T[b], k, 0, tmpA[(size_t)b * c.icap + t], k, 0, k);
     }
   }
   g.run(c.up, c.s, &c.fc_all);
+  // the small far blocks: one fused T_b A T'_q^T per block table slot
+  const void* dA = c.up.put(f.A.v);
+  const int* dicnt = c.up.put(c.icnt[l]);
+  const int* diidx = c.up.put(c.iidx[l]);
+  double* const* dT = c.up.put(T);
+  double* const* dT2 = c.up.put(T2);
+  launch_orth_sandwich(dA, dicnt, diidx, f.nb, c.icap, dT, dT2, c.s);
   c.work.reset();   // stream order: later writes to these temporaries follow the reads
 }
 

@@ -1957,6 +1957,47 @@ void launch_keval_table(const void* v, const int* cnt, const int* idx, int nb, i
   LAUNCH(keval_table_kernel, nb * cap, 128, 0, s, static_cast<const BlkDev*>(v), cnt, idx, cap, mode, sk, base, pts, kp, flag);
 }
 
+// Level-start change of variables on the far blocks (reading R13): A_bq <- T_b A_bq T'_q^T for
+// every IL slot of the level's block table with k_b, k_q <= SW_KMAX, one CTA per slot, the
+// intermediate in shared memory, fixed summation order (the larger blocks go
+// through the DMMA GEMM).  T, T2: per-box k x k factors (ld k) of U_b = Q T, V_b = Q' T'.
+constexpr int SW_KMAX = 64;
+__global__ void __launch_bounds__(256) orth_sandwich_kernel(const BlkDev* __restrict__ v, const int* __restrict__ cnt,
+                                                            const int* __restrict__ idx, int cap,
+                                                            const double* const* __restrict__ T,
+                                                            const double* const* __restrict__ T2) {
+  __shared__ double sX[SW_KMAX * SW_KMAX];
+  const long long slot = blockIdx.x;
+  const int b = (int)(slot / cap), t = (int)(slot % cap);
+  if (t >= cnt[b]) return;
+  const BlkDev blk = v[slot];
+  const int kb = blk.rows, kq = blk.cols;
+  if (kb <= 0 || kq <= 0 || kb > SW_KMAX || kq > SW_KMAX || blk.p == nullptr) return;
+  const int q = idx[slot];
+  const double* Tb = T[b];
+  const double* Tq = T2[q];
+  // X = A T'_q^T  (kb x kq): X[i][j] = sum_l A[i][l] T'_q[j][l]  (A read from global / L1)
+  for (int e = threadIdx.x; e < kb * kq; e += blockDim.x) {
+    const int i = e % kb, j = e / kb;
+    double acc = 0.0;
+    for (int l2 = 0; l2 < kq; ++l2) acc = fma(blk.p[(size_t)l2 * blk.ld + i], Tq[(size_t)l2 * kq + j], acc);
+    sX[j * kb + i] = acc;
+  }
+  __syncthreads();
+  // A = T_b X: A[i][j] = sum_l T_b[i][l] X[l][j]
+  for (int e = threadIdx.x; e < kb * kq; e += blockDim.x) {
+    const int i = e % kb, j = e / kb;
+    double acc = 0.0;
+    for (int l2 = 0; l2 < kb; ++l2) acc = fma(Tb[(size_t)l2 * kb + i], sX[j * kb + l2], acc);
+    blk.p[(size_t)j * blk.ld + i] = acc;
+  }
+}
+
+void launch_orth_sandwich(const void* v, const int* cnt, const int* idx, int nb, int cap, const double* const* T,
+                          const double* const* T2, cudaStream_t s) {
+  LAUNCH(orth_sandwich_kernel, nb * cap, 256, 0, s, static_cast<const BlkDev*>(v), cnt, idx, cap, T, T2);
+}
+
 // ------------------------------------------------------------------------------ copies, norms
 __global__ void copy_tasks_kernel(const CopyTask* __restrict__ tasks) {
   const CopyTask tk = tasks[blockIdx.x];

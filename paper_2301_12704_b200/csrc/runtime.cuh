@@ -23,6 +23,9 @@ void launch_gj(const GJTask* t, int ntasks, int nmax, int mode, cudaStream_t s);
 void launch_pqr(const PqrTask* t, int ntasks, size_t smem_doubles, cudaStream_t s);
 void launch_pqr_cluster(const PqrTask* t, int ntasks, cudaStream_t s);
 void launch_keval(const KEvalTask* t, int ntasks, int ysplit, const double* pts, KernelParams kp, int* flag, cudaStream_t s);
+constexpr int ORTH_SW_KMAX = 64;   // = SW_KMAX of orth_sandwich_kernel
+void launch_orth_sandwich(const void* v, const int* cnt, const int* idx, int nb, int cap, const double* const* T,
+                          const double* const* T2, cudaStream_t s);
 void launch_keval_table(const void* v, const int* cnt, const int* idx, int nb, int cap, int mode, const int* sk,
                         const long long* base, const double* pts, KernelParams kp, int* flag, cudaStream_t s);
 void launch_copy(const CopyTask* t, int ntasks, int ysplit, cudaStream_t s);
