@@ -888,14 +888,39 @@ __global__ void __launch_bounds__(PQR_NT) pqr_tasks_kernel(const PqrTask* __rest
         if (lane == 0) norms[c] = 0.0;
         continue;
       }
-      double s = 0.0;
-      for (int r = lane; r < m; r += 32) s += w[r] * col[r];
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      double n2 = 0.0;
-      for (int r = lane; r < m; r += 32) {
-        const double x = col[r] - s * w[r];
-        col[r] = x;
-        n2 += x * x;
+      double s = 0.0, n2 = 0.0;
+      if (m <= 32 * 16) {
+        // column cached in registers between the dot product and the update (one read, one
+        // write per step; same arithmetic order)
+        double cr[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int r = lane + 32 * u;
+          cr[u] = (r < m) ? col[r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int r = lane + 32 * u;
+          if (r < m) s += w[r] * cr[u];
+        }
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int r = lane + 32 * u;
+          if (r < m) {
+            const double x = cr[u] - s * w[r];
+            col[r] = x;
+            n2 += x * x;
+          }
+        }
+      } else {
+        for (int r = lane; r < m; r += 32) s += w[r] * col[r];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        for (int r = lane; r < m; r += 32) {
+          const double x = col[r] - s * w[r];
+          col[r] = x;
+          n2 += x * x;
+        }
       }
       for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
       if (lane == 0) norms[c] = n2;
@@ -915,6 +940,7 @@ __global__ void __launch_bounds__(PQR_NT) pqr_tasks_kernel(const PqrTask* __rest
 // shared memory when they fit), the pivot search / residual sums / re-orthogonalisation
 // coefficients are combined through DSMEM, and the re-orthogonalisation is row-split.
 constexpr int PQC = 8;
+constexpr int PQR_RC = 32;   // column cached in registers (32 per lane) for m <= 1024
 __global__ void __cluster_dims__(PQC, 1, 1) __launch_bounds__(PQR_NT)
 pqr_cluster_kernel(const PqrTask* __restrict__ tasks, int smem_cap) {
   extern __shared__ double pqs[];
@@ -1073,14 +1099,39 @@ pqr_cluster_kernel(const PqrTask* __restrict__ tasks, int smem_cap) {
         if (lane == 0) norms[c] = 0.0;
         continue;
       }
-      double sacc = 0.0;
-      for (int r = lane; r < m; r += 32) sacc += w[r] * col[r];
-      for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-      double n2 = 0.0;
-      for (int r = lane; r < m; r += 32) {
-        const double x = col[r] - sacc * w[r];
-        col[r] = x;
-        n2 += x * x;
+      double sacc = 0.0, n2 = 0.0;
+      if (m <= 32 * PQR_RC) {
+        // the column stays in registers between the dot product and the update: one read and
+        // one write of it per step instead of two reads and a write (same arithmetic order)
+        double cr[PQR_RC];
+#pragma unroll
+        for (int u = 0; u < PQR_RC; ++u) {
+          const int r = lane + 32 * u;
+          cr[u] = (r < m) ? col[r] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PQR_RC; ++u) {
+          const int r = lane + 32 * u;
+          if (r < m) sacc += w[r] * cr[u];
+        }
+        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+#pragma unroll
+        for (int u = 0; u < PQR_RC; ++u) {
+          const int r = lane + 32 * u;
+          if (r < m) {
+            const double x = cr[u] - sacc * w[r];
+            col[r] = x;
+            n2 += x * x;
+          }
+        }
+      } else {
+        for (int r = lane; r < m; r += 32) sacc += w[r] * col[r];
+        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        for (int r = lane; r < m; r += 32) {
+          const double x = col[r] - sacc * w[r];
+          col[r] = x;
+          n2 += x * x;
+        }
       }
       for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
       if (lane == 0) norms[c] = n2;
