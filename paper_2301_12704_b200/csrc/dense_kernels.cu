@@ -1564,16 +1564,16 @@ hh_panel_cluster_kernel(const HHTask* __restrict__ tasks, int j) {
 // cluster barrier, then every CTA sums the 8 partial vectors and reads row c from its owner
 // through distributed shared memory (double-buffered by column parity, so one barrier per
 // column suffices).  Panels of up to 8 x 256 RPT rows.
-template <int RPT>
-__global__ void __cluster_dims__(HHC_REG, 1, 1) __launch_bounds__(HHR_NT)
+template <int RPT, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(HHR_NT)
 hh_panel_reg_cluster_kernel(const HHTask* __restrict__ tasks, int j) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
-  const HHTask tk = tasks[blockIdx.x / HHC_REG];
+  const HHTask tk = tasks[blockIdx.x / CL];
   const int r = min(tk.n, tk.m);
   if (j >= r) return;                       // uniform over the cluster
   const int nbw = min(HHB, r - j), rows = tk.n - j, ld = tk.lda;
-  const int chunk = (rows + HHC_REG - 1) / HHC_REG;
+  const int chunk = (rows + CL - 1) / CL;
   const int lo = min(rows, rank * chunk), hi = min(rows, lo + chunk);
   double* A = tk.A + j + (size_t)j * ld;
   __shared__ double red[2][HHR_NT / 32][HHB];
@@ -1595,7 +1595,7 @@ hh_panel_reg_cluster_kernel(const HHTask* __restrict__ tasks, int j) {
   for (int c = 0; c < HHB; ++c) {
     if (c < nbw) {
       const int ph = c & 1;
-      const int oc = min(HHC_REG - 1, c / max(chunk, 1));   // owner CTA of row c
+      const int oc = min(CL - 1, c / max(chunk, 1));   // owner CTA of row c
 #pragma unroll
       for (int q = 0; q < RPT; ++q)
         if (lo + tid + HHR_NT * q == c) {
@@ -1625,7 +1625,7 @@ hh_panel_reg_cluster_kernel(const HHTask* __restrict__ tasks, int j) {
       if (tid < HHB) {
         double t = 0.0;
 #pragma unroll
-        for (int qq = 0; qq < HHC_REG; ++qq) t += cl.map_shared_rank(&part[0][0], qq)[ph * HHB + tid];
+        for (int qq = 0; qq < CL; ++qq) t += cl.map_shared_rank(&part[0][0], qq)[ph * HHB + tid];
         tot[ph][tid] = t;
         rc[ph][tid] = cl.map_shared_rank(&rowc[0][0], oc)[ph * HHB + tid];
       }
@@ -2191,8 +2191,11 @@ void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode,
   } else if (mode == 5) {
     // register-resident panel on 8-CTA clusters (rows - j <= 8 x 256 RPT)
     const int chunk = (std::max(nmax - j, 1) + HHC_REG - 1) / HHC_REG;
-    if (chunk <= HHR_NT) LAUNCH(hh_panel_reg_cluster_kernel<1>, ntasks * HHC_REG, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
-    else LAUNCH(hh_panel_reg_cluster_kernel<2>, ntasks * HHC_REG, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
+    if (chunk <= HHR_NT) LAUNCH((hh_panel_reg_cluster_kernel<1, HHC_REG>), ntasks * HHC_REG, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
+    else LAUNCH((hh_panel_reg_cluster_kernel<2, HHC_REG>), ntasks * HHC_REG, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
+  } else if (mode == 6) {
+    // register-resident panel on 2-CTA clusters (rows - j <= 2 x 512)
+    LAUNCH((hh_panel_reg_cluster_kernel<2, 2>), ntasks * 2, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
   } else if (mode == 4) {
     // register-resident panel (rows - j <= 256 RPT); nmax = max rows of the batch
     if (nmax - j <= HHR_NT) LAUNCH(hh_panel_reg_kernel<1>, ntasks, HHR_NT, 0, s, static_cast<const HHTask*>(t), j);
