@@ -257,7 +257,7 @@ class AIFMM:
         lv.pending.add((min(p, q), max(p, q)))
         return ("F", (p, q))
 
-    def _eliminate(self, lv, i):
+    def _eliminate(self, lv, i, skip_schur=False):
         l = lv.l
         m, k = lv.m[i], lv.k[i]
         P = np.zeros((m + k, m + k))
@@ -270,12 +270,17 @@ class AIFMM:
         C = {p: (lv.near[(p, i)], bool(lv.E[p])) for p in nb}      # column x_i
         lv.rec[i] = {"G": G, "m": m, "k": k, "R": R, "C": C}
         W = {q: G[:, :m] @ R[q][0] for q in nb}
-        for p in nb:
-            Cp = C[p][0]
-            for q in nb:
-                kind, key = self._target(lv, p, q)
-                store = {"near": lv.near, "A": lv.A, "F": lv.F}[kind]
-                store[key] = store[key] - Cp @ W[q][:m]
+        # R28: with k = m the orthonormal U_i (R13) is square, P_i^{-1} = [[0, U], [U^T, -U^T K U]]
+        # (V = U, R27): G11 = 0 exactly, so the box makes no Schur update and no fill-in.  Decided
+        # when the box's colour begins (a box the colour's compression fills up keeps its terms,
+        # which are then zero up to rounding).
+        if not skip_schur:
+            for p in nb:
+                Cp = C[p][0]
+                for q in nb:
+                    kind, key = self._target(lv, p, q)
+                    store = {"near": lv.near, "A": lv.A, "F": lv.F}[kind]
+                    store[key] = store[key] - Cp @ W[q][:m]
         for p in nb:
             lv.near[(p, i)] = C[p][0] @ G[:m, m:]           # (X_p|Z_p, y_i) += C G12
         for q in nb:
@@ -291,10 +296,12 @@ class AIFMM:
             for c in range(ncol):
                 cset = {b for b in lv.boxes if self.colour[l][b] == c}
                 S = sorted(p for p in lv.pending if p[0] in cset or p[1] in cset)
+                # R28 is decided when the colour begins (before its compression)
+                full = {i for i in cset if lv.m[i] > 0 and lv.k[i] >= lv.m[i]}
                 if S:
                     self._compress(lv, S)
                 for i in sorted(cset):
-                    self._eliminate(lv, i)
+                    self._eliminate(lv, i, skip_schur=i in full)
                 for i in cset:
                     lv.E[i] = True
             assert not lv.pending and not lv.F, "pending far fill-ins at level end"

@@ -1321,9 +1321,16 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
     for (size_t t0 = 0; t0 < qa.size();) {
       size_t t1 = t0;
       grp_a.clear();
-      while (t1 < qa.size() && qa[t1].first == qa[t0].first) grp_a.push_back(qa[t1++].second);
+      while (t1 < qa.size() && qa[t1].first == qa[t0].first) {
+        const int a = qa[t1++].second;
+        // R28: a box whose basis spans R^m (k = m) when its colour begins (this plan precedes
+        // the colour's compression) has G11 = 0 -- no Schur term, no fill-in
+        static const bool no_r28 = getenv("AIFMM_NO_R28") != nullptr;   // debug toggle
+        if (f.m[cs[a]] && (no_r28 || f.k[cs[a]] < f.m[cs[a]])) grp_a.push_back(a);
+      }
       const int q = qa[t0].first;
       t0 = t1;
+      if (grp_a.empty()) continue;
       const int M = live(f, p), N = live(f, q);
       if (!M || !N) continue;
       Blk T;
@@ -1337,7 +1344,6 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
       P.g.task(T.p, T.ld, M, N, 1.0);
       for (int a : grp_a) {
         const int i = cs[a];
-        if (!f.m[i]) continue;
         const Blk& C = f.nearb.at(f.key(p, i));
         P.fix.push_back({P.g.nterms(), a, wcol_of(P.wcol[a], q)});
         P.g.term(-1.0, C.p, C.ld, 0, nullptr, 0, 0, f.m[i]);   // B patched in eliminate_colour
@@ -1375,6 +1381,19 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   }
   cb.run(c.up, c.s);
   batched_inverse(inv, c.work, c.up, c.s, &c.fc_all);
+  static const bool dbg_g11 = getenv("AIFMM_DEBUG_G11") != nullptr;   // debug: |G11| of full boxes (R28)
+  if (dbg_g11) {
+    for (int i : cs) {
+      const int m = f.m[i], k = f.k[i], n = m + k;
+      if (!m || k < m) continue;
+      std::vector<double> h = d2h(c, f.rec[i].G, (size_t)n * n);
+      double a = 0.0, g = 0.0;
+      for (int cc = 0; cc < m; ++cc)
+        for (int r = 0; r < m; ++r) a = std::max(a, std::fabs(h[(size_t)cc * n + r]));
+      for (double v : h) g = std::max(g, std::fabs(v));
+      fprintf(stderr, "[aifmm g11] level %d box %d m %d k %d max|G11| %.3e max|G| %.3e\n", l, i, m, k, a, g);
+    }
+  }
   static const bool dbg_piv = getenv("AIFMM_DEBUG_PIVOTS") != nullptr;   // debug: largest |P_i^-1| entries
   if (dbg_piv) {
     std::vector<std::pair<double, int>> mx;
@@ -1424,7 +1443,8 @@ static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   //    Schur target: (p,i) with i in the colour is never a target of the colour, whose boxes
   //    are not neighbours)
   for (const auto& fx : P.fix) {
-    const int n = f.m[cs[fx.a]] + f.k[cs[fx.a]];
+    const int i = cs[fx.a];
+    const int n = f.m[i] + f.k[i];
     GemmTerm& t = P.g.term_ref(fx.term);
     t.B = W[fx.a] + (size_t)fx.off * n;
     t.ldb = n;
