@@ -515,7 +515,6 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
 // and the owner of the pivot row swaps in the old row c.  Same pivot rule as gj_panel_kernel
 // (largest |entry|, lowest row on ties).  The interchanges of the full rows, D^{-1} and the
 // B / A[J, :] writes are split over the cluster as well.
-constexpr int GJC = 8;
 struct GjcShared {
   double v[2];
   int idx[2];
@@ -523,6 +522,7 @@ struct GjcShared {
   double rowc[2][GJB];   // row c, if this CTA owns it
   double D[GJB][GJB + 1];
 };
+template <int GJC>
 __global__ void __cluster_dims__(GJC, 1, 1) __launch_bounds__(GJ_NT)
 gj_panel_cluster_kernel(const GJBTask* __restrict__ tasks, int j, int cap_rows) {
   extern __shared__ double gjc_p[];      // own panel rows: cnt x GJB, row-major (ld GJB + 1)
@@ -579,7 +579,7 @@ gj_panel_cluster_kernel(const GJBTask* __restrict__ tasks, int j, int cap_rows) 
         oi = o->idx[ph];
       }
       int oq = lane;
-      for (int off = 4; off > 0; off >>= 1) {   // GJC = 8 lanes
+      for (int off = GJC / 2; off > 0; off >>= 1) {   // GJC lanes
         const double v2 = __shfl_xor_sync(0xffffffffu, ov, off);
         const int i2 = __shfl_xor_sync(0xffffffffu, oi, off);
         const int q2 = __shfl_xor_sync(0xffffffffu, oq, off);
@@ -2107,11 +2107,24 @@ void launch_gj(const GJTask* t, int ntasks, int nmax, int mode, cudaStream_t s) 
   }
 }
 
-void launch_gj_panel_cluster(const void* t, int ntasks, int j, int nmax, cudaStream_t s) {
-  const int cap = (std::max(nmax - j, 1) + GJC - 1) / GJC;
+template <int CL>
+static void launch_gj_panel_cluster_cl(const void* t, int ntasks, int j, int nmax, cudaStream_t s) {
+  const int cap = (std::max(nmax - j, 1) + CL - 1) / CL;
   const size_t smem = (size_t)cap * (GJB + 1) * sizeof(double);
-  ensure_dyn_smem(gj_panel_cluster_kernel, smem);
-  LAUNCH(gj_panel_cluster_kernel, ntasks * GJC, GJ_NT, smem, s, static_cast<const GJBTask*>(t), j, cap);
+  ensure_dyn_smem(gj_panel_cluster_kernel<CL>, smem);
+  LAUNCH(gj_panel_cluster_kernel<CL>, ntasks * CL, GJ_NT, smem, s, static_cast<const GJBTask*>(t), j, cap);
+}
+// cluster size by batch: 8 CTAs per matrix for a few matrices, fewer when 8 x the batch would
+// take several waves of the 148 SMs (the row slices must still fit shared memory)
+void launch_gj_panel_cluster(const void* t, int ntasks, int j, int nmax, cudaStream_t s) {
+  static const int force = getenv("AIFMM_GJ_CL") ? atoi(getenv("AIFMM_GJ_CL")) : 0;   // debug toggle
+  const auto fits = [&](int cl) { return (size_t)((nmax + cl - 1) / cl) * (GJB + 1) * sizeof(double) <= 200 * 1024; };
+  int cl = 8;
+  if (force) cl = force;
+  else if (ntasks * 8 > 2 * 148 && fits(4)) cl = (ntasks * 4 > 2 * 148 && fits(2)) ? 2 : 4;
+  if (cl == 2) launch_gj_panel_cluster_cl<2>(t, ntasks, j, nmax, s);
+  else if (cl == 4) launch_gj_panel_cluster_cl<4>(t, ntasks, j, nmax, s);
+  else launch_gj_panel_cluster_cl<8>(t, ntasks, j, nmax, s);
 }
 void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s) {
   const int elems = (160 * 1024) / 8;

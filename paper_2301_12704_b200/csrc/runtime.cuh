@@ -549,7 +549,7 @@ inline void batched_inverse(const std::vector<InvReq>& reqs, Pool& work, Uploade
   const void* dt = up.put(tb.data(), tb.size());
   // few matrices: 8-CTA clusters per matrix (row slices in shared memory); many: one CTA each
   static const bool gj_single = getenv("AIFMM_GJ_SINGLE") != nullptr;   // debug toggle
-  const bool cluster = !gj_single && (int)big.size() * 4 < 148 * 2 && nmax <= 8 * 700;
+  const bool cluster = !gj_single && (int)big.size() <= 148 && nmax <= 8 * 700;
   for (int j = 0; j < nmax; j += GJ_PANEL) {
     if (cluster) launch_gj_panel_cluster(dt, (int)big.size(), j, nmax, s);
     else launch_gj_panel(dt, (int)big.size(), j, s);

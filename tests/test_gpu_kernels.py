@@ -103,3 +103,32 @@ def test_tri_root_two_cta_register_variant():
     env = dict(os.environ, AIFMM_HH_REG2="1", AIFMM_TSQR_MMAX="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("cl", [2, 4])
+def test_pivot_inverse_cluster_sizes(cl):
+    """The Gauss-Jordan cluster panel with 2- and 4-CTA clusters (chosen for larger batches;
+    forced here through AIFMM_GJ_CL, read once per process, so it runs in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, %r)\n"
+        "from paper_2301_12704_b200 import aifmm as G\n"
+        "def saddle(m, k, seed):\n"
+        "    rng = np.random.default_rng(seed)\n"
+        "    K = rng.standard_normal((m, m)) + 4 * np.eye(m)\n"
+        "    U = np.linalg.qr(rng.standard_normal((m, k)))[0]\n"
+        "    V = np.linalg.qr(rng.standard_normal((m, k)))[0]\n"
+        "    P = np.zeros((m + k, m + k)); P[:m, :m], P[:m, m:], P[m:, :m] = K, U, V.T\n"
+        "    return P\n"
+        "for m, k in ((250, 90), (700, 300)):\n"
+        "    P = saddle(m, k, 3)\n"
+        "    Gi = G.debug_inverse(torch.from_numpy(P).cuda()).cpu().numpy()\n"
+        "    cond = np.linalg.cond(P)\n"
+        "    assert np.linalg.norm(P @ Gi - np.eye(m + k)) <= 1e-12 * cond, (m, k)\n"
+        "print('ok')\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    env = dict(os.environ, AIFMM_GJ_CL=str(cl))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
