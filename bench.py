@@ -291,7 +291,8 @@ def run_ours(args, cfg):
                    "l2": "flushed (256 MB write) between steps"},
         "phase_ms": {"build": tb / args.steps, "factor": tf / args.steps, "solve_16rhs": ts / args.steps},
         "rel_residual_4096_rows": res,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(pts.nbytes + b.nbytes),
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": [round(t * 1e3, 2) for t in e2e_t],
+                "h2d_bytes_per_step": int(pts.nbytes + b.nbytes),
                 "d2h_bytes_per_step": int(b.nbytes), "includes": "H2D points, build, factor, H2D B, solve, D2H X"},
         "gpu_launches": int(launches / args.steps),
         "roofline": roof,
