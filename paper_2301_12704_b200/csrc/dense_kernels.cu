@@ -1808,9 +1808,11 @@ hh_panel_cluster_smem_kernel(const HHTask* __restrict__ tasks, int j, int cap_ro
 // shared memory, the products run on DMMA (mma.sync m8n8k4 f64).  Fixed summation order.
 struct HHUTile { int task, n0; };
 constexpr int HHU_NT = 256;
-constexpr int HHU_BN = 64, HHU_RK = 32, HHU_ST = 3;   // column block, row chunk, pipeline stages
+constexpr int HHU_BN = 64, HHU_RK = 32;   // column block, row chunk (pipeline stages: template)
 constexpr int HHU_LV = HHB + 4, HHU_LC = HHU_BN + 4;  // padded rows (stride = 4 mod 16: no bank conflicts)
-constexpr size_t HHU_SMEM = sizeof(double) * ((size_t)HHU_ST * HHU_RK * (HHU_LV + HHU_LC) + (size_t)HHB * HHU_LC);
+template <int HHU_ST>
+constexpr size_t hhu_smem() { return sizeof(double) * ((size_t)HHU_ST * HHU_RK * (HHU_LV + HHU_LC) + (size_t)HHB * HHU_LC); }
+template <int HHU_ST>
 __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restrict__ tasks,
                                                            const HHUTile* __restrict__ tiles, int j) {
   extern __shared__ __align__(16) double hhu_smem[];
@@ -1940,8 +1942,14 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
   cp_async_wait<0>();
 }
 void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s) {
-  ensure_dyn_smem(hh_update_kernel, HHU_SMEM);
-  LAUNCH(hh_update_kernel, ntiles, HHU_NT, HHU_SMEM, s, static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j);
+  static const int st = getenv("AIFMM_HHU_ST") ? atoi(getenv("AIFMM_HHU_ST")) : 3;   // experiment toggle
+  if (st == 2) {
+    ensure_dyn_smem(hh_update_kernel<2>, hhu_smem<2>());
+    LAUNCH(hh_update_kernel<2>, ntiles, HHU_NT, hhu_smem<2>(), s, static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j);
+  } else {
+    ensure_dyn_smem(hh_update_kernel<3>, hhu_smem<3>());
+    LAUNCH(hh_update_kernel<3>, ntiles, HHU_NT, hhu_smem<3>(), s, static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j);
+  }
 }
 
 // M = R^T (m x r) from the upper triangle of the factored A (n x m, lda)
