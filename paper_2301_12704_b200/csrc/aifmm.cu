@@ -1469,10 +1469,19 @@ static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   g_prof.hstart();
   GemmBatch gf;
   std::vector<std::pair<long long, Blk>> fresh;
+  {
+    size_t nf = 0;
+    for (size_t a = 0; a < cs.size(); ++a) nf += P.nbs[a].size() + P.wcol[a].size() + 1;
+    fresh.reserve(nf);
+  }
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];
     const int m = f.m[i], k = f.k[i], n = m + k;
     Rec& r = f.rec[i];
+    r.C.reserve(P.nbs[a].size());
+    r.Ckind_z.reserve(P.nbs[a].size());
+    r.R.reserve(P.wcol[a].size());
+    r.Rkind_y.reserve(P.wcol[a].size());
     for (int p : P.nbs[a]) {
       const Blk& C = f.nearb.at(f.key(p, i));
       r.C.push_back({p, C});
