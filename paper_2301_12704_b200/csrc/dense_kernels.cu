@@ -178,6 +178,7 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmTerm* __restrict
 
 template __global__ void gemm_tasks_kernel<64, 64>(const GemmTask*, const GemmTerm*, const GemmTile*);
 template __global__ void gemm_tasks_kernel<64, 64, 5>(const GemmTask*, const GemmTerm*, const GemmTile*);
+template __global__ void gemm_tasks_kernel<64, 128, 2>(const GemmTask*, const GemmTerm*, const GemmTile*);
 template __global__ void gemm_tasks_kernel<64, 64, 6>(const GemmTask*, const GemmTerm*, const GemmTile*);
 template __global__ void gemm_tasks_kernel<32, 32>(const GemmTask*, const GemmTerm*, const GemmTile*);
 template __global__ void gemm_tasks_kernel<64, 32>(const GemmTask*, const GemmTerm*, const GemmTile*);
@@ -2097,6 +2098,10 @@ void launch_gemm(int tileclass, const GemmTask* t, const GemmTerm* tm, const Gem
     init = true;
   }
   switch (tileclass) {
+    case 4:   // 64 x 128 tiles, 8 warps (same per-element accumulation order as 64 x 64)
+      ensure_dyn_smem(gemm_tasks_kernel<64, 128, 2>, gemm_smem<64, 128>());
+      LAUNCH((gemm_tasks_kernel<64, 128, 2>), ntiles, 256, (gemm_smem<64, 128>()), s, t, tm, tiles);
+      break;
     case 0: LAUNCH((gemm_tasks_kernel<32, 32>), ntiles, 32, (gemm_smem<32, 32>()), s, t, tm, tiles); break;
     case 1: LAUNCH((gemm_tasks_kernel<64, 32>), ntiles, 64, (gemm_smem<64, 32>()), s, t, tm, tiles); break;
     case 2: LAUNCH((gemm_tasks_kernel<32, 64>), ntiles, 64, (gemm_smem<32, 64>()), s, t, tm, tiles); break;

@@ -400,13 +400,15 @@ class GemmBatch {
         red_tasks.push_back(r);
       }
     }
-    std::vector<GemmTile> tl[4];
+    std::vector<GemmTile> tl[5];
+    static const bool wide = getenv("AIFMM_GEMM_WIDE") != nullptr;   // experiment toggle
     for (size_t t = 0; t < tasks_.size(); ++t) {
       const GemmTask& k = tasks_[t];
       if (k.M <= 0 || k.N <= 0) continue;
       int cls = (k.M <= 32 ? 0 : 1) + (k.N <= 32 ? 0 : 2);
-      // class ids: 0 -> 32x32, 1 -> 64x32, 2 -> 32x64, 3 -> 64x64
-      int bm = (cls & 1) ? 64 : 32, bn = (cls & 2) ? 64 : 32;
+      // class ids: 0 -> 32x32, 1 -> 64x32, 2 -> 32x64, 3 -> 64x64, 4 -> 64x128
+      if (wide && cls == 3 && k.N > 64) cls = 4;
+      int bm = (cls & 1) || cls == 4 ? 64 : 32, bn = cls == 4 ? 128 : ((cls & 2) ? 64 : 32);
       for (int m0 = 0; m0 < k.M; m0 += bm)
         for (int n0 = 0; n0 < k.N; n0 += bn) tl[cls].push_back(GemmTile{(int)t, m0, n0, 0});
       if (fc) {
@@ -424,11 +426,11 @@ class GemmBatch {
       }
     }
     size_t need = tasks_.size() * sizeof(GemmTask) + terms_.size() * sizeof(GemmTerm) + 4 * 256;
-    for (int c = 0; c < 4; ++c) need += tl[c].size() * sizeof(GemmTile);
+    for (int c = 0; c < 5; ++c) need += tl[c].size() * sizeof(GemmTile);
     up.reserve(need);
     GemmTask* dt = up.put(tasks_);
     GemmTerm* dm = terms_.empty() ? nullptr : up.put(terms_);
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 5; ++c) {
       if (tl[c].empty()) continue;
       GemmTile* dtl = up.put(tl[c]);
       launch_gemm(c, dt, dm, dtl, (int)tl[c].size(), s);
