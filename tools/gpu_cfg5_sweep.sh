@@ -1,6 +1,5 @@
 #!/bin/bash
-# config-5 preconditioner quality vs N (symmetric reading R27 vs independent sides)
+# config-5 preconditioner quality vs N (current defaults)
 for n in 65536 131072 262144; do
-  echo "sym n=$n $(timeout 900 python tools/gpu_cfg5_diag.py $n 128 2>&1 | grep '^{' | tail -1)"
+  echo "n=$n $(timeout 900 python tools/gpu_cfg5_diag.py $n 128 2>&1 | grep '^{' | tail -1)"
 done
-echo "asym n=131072 $(AIFMM_ASYMMETRIC=1 timeout 900 python tools/gpu_cfg5_diag.py 131072 128 2>&1 | grep '^{' | tail -1)"
