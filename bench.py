@@ -1,10 +1,12 @@
 """bench.py — AIFMM factor+solve throughput on B200 (BASELINE.json metric).
 
-Workload (N=1): BASELINE config 2 — 2D, N = 65,536 uniform random points in [-1,1]^2
-(seed 1), A_ij = log|x_i - x_j|, A_ii = 10, leaf 64, tol 1e-10, 16 RHS.  One step = the whole
-hot path: aifmm_build (tree, lists, colours, NNCA), aifmm_factor
-(colour-batched Alg. 3) and aifmm_solve (Alg. 4, 16 RHS).  Inputs are resident in HBM when
-the timed region starts; L2 (126 MB) is flushed by writing a 256 MB buffer between steps.
+Workload (N=1): BASELINE config 3, the largest configuration that fits one GPU — 2D,
+N = 1,048,576 uniform random points in [-1,1]^2 (seed 2), Matern-1/2 A_ij = exp(-|x_i-x_j|/0.1)
+with A_ii = 1 + 1e-2, leaf 128, tol 1e-8, 1 RHS.  One step = the whole hot path (SURVEY §8(a)
+rows a1-a7): aifmm_build (tree, lists, colours, NNCA), aifmm_factor (colour-batched Alg. 3)
+and aifmm_solve (Alg. 4).  Inputs are resident in HBM when the timed region starts; L2
+(126 MB) is flushed by writing a 256 MB buffer between steps (the step's working set is
+~160 GB anyway).  `--cfg 2` selects BASELINE config 2 (N = 65,536, log r, 16 RHS).
 
 N>1 (torchrun): every rank factors its own independent instance of the workload (rank-offset
 seed; weak scaling, no data-path collective).
@@ -32,8 +34,9 @@ from paper_2301_12704_b200 import dist as D  # noqa: E402
 
 METRIC = "AIFMM factor+solve unknowns/sec"
 UNIT = "unknowns/s"
-CFG_INDEX = 1                 # BASELINE configs[1] (config 2): the metric's workload on one GPU
-SAMPLE_N = 16384              # oracle sample size (same distribution, kernel, leaf, tol, nrhs)
+CFG_DEFAULT = 3               # BASELINE config 3: the largest single-GPU configuration
+SAMPLE_N = {2: 16384, 3: 4096}   # oracle sample size (same distribution, kernel, leaf, tol, nrhs)
+KERNEL_NAMES = {0: "log r", 1: "exp(-r/ell)", 2: "1/r"}
 
 
 def _peaks():
@@ -121,30 +124,46 @@ def _cores():
         return os.cpu_count() or 1
 
 
+def _config_dict(cfg, **extra):
+    d = {"workload": cfg.name, "n": cfg.n, "nrhs": cfg.nrhs,
+         "kernel": f"{KERNEL_NAMES[cfg.kernel_id]}, A_ii={cfg.diag:g}" + (f", ell={cfg.ell:g}" if cfg.kernel_id == 1 else ""),
+         "leaf": cfg.leaf_size, "tol": cfg.tol}
+    d.update(extra)
+    return d
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    sn = SAMPLE_N[args.cfg]
     times = []
     for _ in range(args.warmup):          # warm imports / BLAS threads on a tiny instance
         _oracle_sample(cfg, 1024)
     for _ in range(max(1, args.steps)):
-        r = _oracle_sample(cfg, SAMPLE_N)
+        r = _oracle_sample(cfg, sn)
         times.append(r)
     fs = [t["factor_s"] + t["solve_s"] for t in times]
-    value = SAMPLE_N / float(np.mean(fs))
+    value = sn / float(np.mean(fs))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean([t["build_s"] + t["factor_s"] + t["solve_s"] for t in times])),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "n": cfg.n, "nrhs": cfg.nrhs, "kernel": "log r, A_ii=10",
-                   "leaf": cfg.leaf_size, "tol": cfg.tol, "sample_n": SAMPLE_N},
+        "config": _config_dict(cfg, sample_n=sn),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cores(), "kind": "oracle",
-                         "sample": f"first {SAMPLE_N} points of the config-2 draw (seed 1), same kernel/leaf/tol/16 RHS"},
+                         "sample": f"first {sn} points of the {cfg.name} draw (seed {cfg.seed}), same kernel/leaf/tol/{cfg.nrhs} RHS"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "phase_s": {k: float(np.mean([t[k] for t in times])) for k in ("build_s", "factor_s", "solve_s")},
     }
     print(json.dumps(line), flush=True)
+
+
+def _phase_roofline(name, kernels, bound, work, ms, peak, unit, launches=None):
+    achieved = (work / (ms / 1e3)) / (1e12 if unit == "TFLOP/s" else 1e9) if ms > 0 else None
+    return {"phase": name, "kernels": kernels, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": (achieved / peak) if (achieved and peak) else None, "device_ms_per_step": ms,
+            ("algorithmic_tflop_per_step" if unit == "TFLOP/s" else "algorithmic_gb_per_step"):
+                work / (1e12 if unit == "TFLOP/s" else 1e9)}
 
 
 def run_ours(args, cfg):
@@ -164,8 +183,8 @@ def run_ours(args, cfg):
     A.set_stream(stream.cuda_stream)
 
     # N > 1: every rank factors its own independent instance of the workload (same
-    # distribution, kernel, leaf size, tol, nrhs; rank-offset seed): weak scaling over
-    # independent problems, no data-path collective
+    # distribution, kernel, leaf size, tol, nrhs; rank-offset seed): independent replicas, no
+    # data-path collective
     cfg_r = D.instance_config(cfg, rank)
     pts, b = W.make(cfg_r)
     P = torch.from_numpy(pts).to(dev)
@@ -196,8 +215,11 @@ def run_ours(args, cfg):
     clocks.start()
     A.reset_counters()
     tb = tf = ts = 0.0
-    schur_ms = schur_flops = schur_bytes = schur_launches = 0.0
+    acc = {}
     launches = 0.0
+    keys = ("schur_ms", "schur_flops", "schur_bytes", "schur_launches", "pivot_ms", "pivot_flops", "pivot_bytes",
+            "tri_ms", "tri_flops", "tri_bytes", "pqr_ms", "pqr_bytes", "redir_ms", "redir_flops", "redir_bytes",
+            "factor_flops", "max_rank", "compressions", "device_bytes", "host_syncs")
     for _ in range(args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
@@ -207,26 +229,31 @@ def run_ours(args, cfg):
         tf += e[1].elapsed_time(e[2])
         ts += e[2].elapsed_time(e[3])
         st = A.stats()
-        schur_ms += st["schur_ms"]
-        schur_flops += st["schur_flops"]
-        schur_bytes += st["schur_bytes"]
-        schur_launches += st["schur_launches"]
+        for k in keys:
+            acc[k] = acc.get(k, 0.0) + st[k]
         launches += st["launches"]
         A.reset_counters()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    step_ms = (tb + tf + ts) / args.steps
-    fs_ms = (tf + ts) / args.steps
+    K = float(args.steps)
+    step_ms = (tb + tf + ts) / K
+    fs_ms = (tf + ts) / K
     fs_ms, step_ms = D.max_over_ranks([fs_ms, step_ms], dev)
     value = D.aggregate_throughput(cfg.n, world, fs_ms / 1e3)
 
+    # correctness guard on the last device result: direct-sum residual on the GPU (row a9,
+    # aifmm_residual) over the 4096 sampled rows
+    Xu = X.t()
+    res = A.residual(Xu, B, W.residual_rows(cfg.n, cfg_r.seed))
+
     # end-to-end: host points + host B through the public API, copies inside the region
+    # (one untimed warm-up, then the mean of up to 3 timed runs)
     pts_h = torch.from_numpy(pts).pin_memory()
     Bh = np.asfortranarray(b.copy())
     torch.cuda.synchronize()
     e2e_t = []
-    for _ in range(max(1, min(args.steps, 3))):
+    for it in range(1 + max(1, min(args.steps, 3))):
         A.free()
         flush.fill_(1.0)
         torch.cuda.synchronize()
@@ -236,66 +263,75 @@ def run_ours(args, cfg):
         A.factor()
         Xh = A.solve_host(Bh.copy())
         torch.cuda.synchronize()
-        e2e_t.append(time.perf_counter() - t0)
+        if it > 0:
+            e2e_t.append(time.perf_counter() - t0)
     e2e_value = D.aggregate_throughput(cfg.n, world, D.max_over_ranks([float(np.mean(e2e_t))], dev)[0])
-
-    # correctness guard on the last device result (sampled direct-sum residual)
-    res = None
-    if rank == 0:
-        from oracle import dense
-        rows = W.residual_rows(cfg.n, cfg_r.seed)
-        res = dense.residual(pts, cfg.kernel_id, cfg.kparams, X.t().cpu().numpy(), b, rows)
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     pk = _peaks()
-    achieved = (schur_flops / (schur_ms / 1e3)) / 1e12 if schur_ms > 0 else None
-    peak = pk.get("fp64_dgemm_tflops") or (pk["bf16_tflops"] * 45.0 / 2250.0 if pk["bf16_tflops"] else None)
+    fp64 = pk.get("fp64_dgemm_tflops") or (pk["bf16_tflops"] * 45.0 / 2250.0 if pk["bf16_tflops"] else None)
+    hbm = pk.get("hbm_gbs")
     # DRAM traffic per Schur launch from the committed `ncu --set full` capture of exactly these
     # launches (NVTX range "schur"; tools/ncu_kernel_traffic.py), next to the algorithmic bytes
     traffic, ncu_src = None, None
     try:
-        nc = json.load(open(os.path.join(ROOT, "profiles", "r01_schur_gemm_ncu.json")))
+        nc = json.load(open(os.path.join(ROOT, "profiles", f"r02_schur_gemm_ncu_cfg{args.cfg}.json")))
         traffic, ncu_src = nc.get("dram_bytes_per_launch"), nc
     except Exception:
         pass
+    sch_ms = acc["schur_ms"] / K
+    achieved = (acc["schur_flops"] / K) / (sch_ms / 1e3) / 1e12 if sch_ms > 0 else None
     roof = {
         "kernel": "gemm_tasks_kernel (Schur-complement updates, DMMA)",
-        "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": (achieved / peak) if (achieved and peak) else None,
+        "bound": "tensor", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+        "frac": (achieved / fp64) if (achieved and fp64) else None,
         "traffic": traffic,
-        "traffic_source": ("profiles/r01_schur_gemm_ncu.json: mean dram__bytes_read.sum + dram__bytes_write.sum "
-                           "over %d captured Schur launches" % ncu_src["launches_captured"]) if ncu_src else None,
-        "algorithmic_bytes_per_launch": (schur_bytes / schur_launches) if schur_launches else None,
-        "algorithmic_flop_per_launch": (schur_flops / schur_launches) if schur_launches else None,
-        "launches_per_step": schur_launches / args.steps,
-        "peak_source": "cuBLAS FP64 DGEMM 8192^3 measured on this pool (profiles/r01_fp64_dgemm_peak.json); "
-                       "bf16 measured x 45/2250 nominal ratio = %.1f" % (pk["bf16_tflops"] * 45.0 / 2250.0 if pk["bf16_tflops"] else float("nan")),
-        "schur_ms_per_step": schur_ms / args.steps, "schur_gflop_per_step": schur_flops / args.steps / 1e9,
+        "traffic_source": (f"profiles/r02_schur_gemm_ncu_cfg{args.cfg}.json: mean dram__bytes_read.sum + "
+                           f"dram__bytes_write.sum over {ncu_src['launches_captured']} captured Schur launches") if ncu_src else None,
+        "algorithmic_bytes_per_launch": (acc["schur_bytes"] / acc["schur_launches"]) if acc["schur_launches"] else None,
+        "algorithmic_flop_per_launch": (acc["schur_flops"] / acc["schur_launches"]) if acc["schur_launches"] else None,
+        "launches_per_step": acc["schur_launches"] / K,
+        "peak_source": "FP64 (DMMA) peak = cuBLAS DGEMM 8192^3 measured on this pool "
+                       "(profiles/r01_fp64_dgemm_peak.json); MEASURED_PEAKS.json has no FP64 entry",
+        "schur_ms_per_step": sch_ms, "schur_gflop_per_step": acc["schur_flops"] / K / 1e9,
     }
+    phases = [
+        _phase_roofline("pivot factorisation (P_i^-1, P:753)", "gj_small_kernel / gj_panel_* + DMMA GEMM", "tensor",
+                        acc["pivot_flops"] / K, acc["pivot_ms"] / K, fp64, "TFLOP/s"),
+        _phase_roofline("RRQR stage 1 (Householder of W^T, R8b)", "hh_panel_* + hh_update_kernel", "hbm",
+                        acc["tri_bytes"] / K, acc["tri_ms"] / K, hbm, "GB/s"),
+        _phase_roofline("RRQR stage 2 (truncated pivoted QR, P:841-849)", "pqr_tasks_kernel / pqr_cluster_kernel", "hbm",
+                        acc["pqr_bytes"] / K, acc["pqr_ms"] / K, hbm, "GB/s"),
+        _phase_roofline("redirection (P:877-882, P:1010-1014, P:1078-1082)", "gemm_tasks_kernel", "hbm",
+                        acc["redir_bytes"] / K, acc["redir_ms"] / K, hbm, "GB/s"),
+    ]
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        r = _oracle_sample(cfg, SAMPLE_N)
-        cpu = {"value": SAMPLE_N / (r["factor_s"] + r["solve_s"]), "unit": UNIT, "cores": _cores(), "kind": "oracle",
-               "sample": f"first {SAMPLE_N} points of the config-2 draw (seed 1), same kernel/leaf/tol/16 RHS; "
+        sn = SAMPLE_N[args.cfg]
+        r = _oracle_sample(cfg, sn)
+        cpu = {"value": sn / (r["factor_s"] + r["solve_s"]), "unit": UNIT, "cores": _cores(), "kind": "oracle",
+               "sample": f"first {sn} points of the {cfg.name} draw (seed {cfg.seed}), same kernel/leaf/tol/{cfg.nrhs} RHS; "
                          f"factor {r['factor_s']:.1f}s solve {r['solve_s']:.1f}s"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "n": cfg.n, "nrhs": cfg.nrhs, "kernel": "log r, A_ii=10",
-                   "leaf": cfg.leaf_size, "tol": cfg.tol,
-                   "parallelism": "1 GPU" if world == 1 else f"{world} independent instances (one per GPU)",
-                   "l2": "flushed (256 MB write) between steps"},
-        "phase_ms": {"build": tb / args.steps, "factor": tf / args.steps, "solve_16rhs": ts / args.steps},
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(cfg, parallelism="1 GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+                               l2="flushed (256 MB write) between steps; working set > L2"),
+        "phase_ms": {"build": tb / K, "factor": tf / K, "solve": ts / K},
         "rel_residual_4096_rows": res,
+        "factor_tflop_per_step": acc["factor_flops"] / K / 1e12,
+        "max_rank": acc["max_rank"] / K, "compressions_per_step": acc["compressions"] / K,
+        "device_gb": acc["device_bytes"] / K / 1e9, "host_syncs_per_step": acc["host_syncs"] / K,
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": [round(t * 1e3, 2) for t in e2e_t],
                 "h2d_bytes_per_step": int(pts.nbytes + b.nbytes),
-                "d2h_bytes_per_step": int(b.nbytes), "includes": "H2D points, build, factor, H2D B, solve, D2H X"},
-        "gpu_launches": int(launches / args.steps),
+                "d2h_bytes_per_step": int(b.nbytes), "includes": "H2D points, build, factor, H2D B, solve, D2H X; warm-up run excluded"},
+        "gpu_launches": int(launches / K),
         "roofline": roof,
+        "roofline_phases": phases,
         "cpu_baseline": cpu,
         "clocks": clk,
     }
@@ -309,10 +345,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--cfg", type=int, default=CFG_DEFAULT, choices=[2, 3], help="BASELINE config number")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    cfg = W.CONFIGS[CFG_INDEX]
+    cfg = W.CONFIGS[args.cfg - 1]
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -122,8 +122,19 @@ int aifmm_matvec(const double* X, double* Y, int nrhs);
 int aifmm_gmres(const double* b, double* x, int restart, double rtol, int maxit, int precond,
                 int* iters, double* relres);
 
+/* aifmm_residual — row a9 (verification; not part of the timed path): the relative residual
+ *   ||A X - B||_F / ||B||_F of a solution X over the sampled rows, with A_ij = K(x_i, x_j) and
+ *   A_ii = diag evaluated exactly by direct sum (the problem statement P:105-111; the paper's
+ *   accuracy metric is a relative error in the 2-norm).
+ *   X, B   device, n x nrhs column-major (ld n), user point order; read only.
+ *   rows   host int64[nrows] user row indices (NULL: every row, nrows ignored).
+ *   rel    host out.  Deterministic (fixed reduction order).
+ * Requires aifmm_build.  Errors: ESTATE, EINVALID_ARG (NULL pointer, nrhs < 1, row out of
+ * range), ECUDA, EOOM.  Cost: nrows x n kernel evaluations per right-hand side group of 4. */
+int aifmm_residual(const double* X, const double* B, int nrhs, const int64_t* rows, int64_t nrows, double* rel);
+
 /* aifmm_stats — host double[AIFMM_NSTATS], see the AIFMM_STAT_* indices. */
-#define AIFMM_NSTATS 16
+#define AIFMM_NSTATS 28
 #define AIFMM_STAT_BUILD_MS        0
 #define AIFMM_STAT_FACTOR_MS       1
 #define AIFMM_STAT_SOLVE_MS        2
@@ -140,6 +151,22 @@ int aifmm_gmres(const double* b, double* x, int restart, double rtol, int maxit,
 #define AIFMM_STAT_SCHUR_LAUNCHES 13
 #define AIFMM_STAT_SOLVE_BYTES    14
 #define AIFMM_STAT_HOST_SYNCS     15
+/* per-phase device time (CUDA events around the phase's launches, recorded when
+ * aifmm_set_timing(1)) and algorithmic FLOPs / bytes of the last factorization:
+ * pivot factorisations (P_i of P:753), Householder first stage and truncated pivoted QR of the
+ * RRQR, redirection GEMMs */
+#define AIFMM_STAT_PIVOT_MS       16
+#define AIFMM_STAT_PIVOT_FLOPS    17
+#define AIFMM_STAT_PIVOT_BYTES    18
+#define AIFMM_STAT_TRI_MS         19
+#define AIFMM_STAT_TRI_FLOPS      20
+#define AIFMM_STAT_TRI_BYTES      21
+#define AIFMM_STAT_PQR_MS         22
+#define AIFMM_STAT_PQR_FLOPS      23
+#define AIFMM_STAT_PQR_BYTES      24
+#define AIFMM_STAT_REDIR_MS       25
+#define AIFMM_STAT_REDIR_FLOPS    26
+#define AIFMM_STAT_REDIR_BYTES    27
 int aifmm_stats(double* out);
 /* aifmm_reset_counters — zero the launch / FLOP / time counters. */
 int aifmm_reset_counters(void);

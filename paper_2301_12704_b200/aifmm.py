@@ -22,10 +22,13 @@ SYMBOLS = ["aifmm_build", "aifmm_set_compression_tol", "aifmm_factor", "aifmm_so
            "aifmm_solve_host", "aifmm_free", "aifmm_last_error", "aifmm_set_stream",
            "aifmm_get_tree", "aifmm_get_level_offsets", "aifmm_get_lists", "aifmm_get_colours",
            "aifmm_get_ranks", "aifmm_stats", "aifmm_reset_counters", "aifmm_set_timing",
-           "aifmm_debug_inverse", "aifmm_debug_tri_root", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres"]
+           "aifmm_debug_inverse", "aifmm_debug_tri_root", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres",
+           "aifmm_residual"]
 STAT_NAMES = ["build_ms", "factor_ms", "solve_ms", "levels", "top_size", "factor_flops",
               "schur_flops", "schur_ms", "launches", "compressions", "max_rank", "device_bytes",
-              "schur_bytes", "schur_launches", "solve_bytes", "host_syncs"]
+              "schur_bytes", "schur_launches", "solve_bytes", "host_syncs",
+              "pivot_ms", "pivot_flops", "pivot_bytes", "tri_ms", "tri_flops", "tri_bytes",
+              "pqr_ms", "pqr_flops", "pqr_bytes", "redir_ms", "redir_flops", "redir_bytes"]
 
 
 class AIFMMError(RuntimeError):
@@ -66,6 +69,7 @@ def load(path: str = LIB_PATH):
     lib.aifmm_matvec_build.argtypes = [D]
     lib.aifmm_matvec.argtypes = [P, P, I]
     lib.aifmm_gmres.argtypes = [P, P, I, D, I, I, P, P]
+    lib.aifmm_residual.argtypes = [P, P, I, P, I64, P]
     _lib = lib
     return lib
 
@@ -79,12 +83,28 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
+_bound_stream = None
+
+
+def _bind_stream():
+    """Run the library on torch's current CUDA stream, so that the tensors this module prepares
+    (.to / .contiguous / .clone on that stream) are complete before the library reads them and
+    the library's results are ordered before torch's later work (no cross-stream race)."""
+    global _bound_stream
+    import torch
+    s = torch.cuda.current_stream().cuda_stream
+    if s != _bound_stream:
+        _check(load().aifmm_set_stream(ctypes.c_void_p(s)))
+        _bound_stream = s
+
+
 def build(points, kernel_id: int, kparams, leaf_size: int, tol: float):
     """points: torch.cuda float64 tensor (n, d), any layout (made contiguous)."""
     import torch
     lib = load()
     if not (isinstance(points, torch.Tensor) and points.is_cuda):
         raise TypeError("points must be a CUDA tensor (device memory)")
+    _bind_stream()
     pts = points.to(torch.float64).contiguous()
     kp = np.asarray(kparams, dtype=np.float64)
     _check(lib.aifmm_build(ctypes.c_void_p(pts.data_ptr()), pts.shape[0], pts.shape[1], int(kernel_id),
@@ -96,6 +116,7 @@ def set_compression_tol(tol_c: float):
 
 
 def factor():
+    _bind_stream()
     _check(load().aifmm_factor())
 
 
@@ -105,6 +126,7 @@ def solve(B):
     lib = load()
     one = B.dim() == 1
     Bm = B[:, None] if one else B
+    _bind_stream()
     # (nrhs, n) row-major == (n, nrhs) column-major; always a fresh buffer (the library solves in
     # place, and for one column .t().contiguous() would alias the caller's tensor)
     Bc = Bm.to(torch.float64).t().contiguous().clone()
@@ -115,6 +137,7 @@ def solve(B):
 
 def solve_device_ptr(ptr: int, nrhs: int):
     """In-place solve of a column-major n x nrhs device buffer given by its address."""
+    _bind_stream()
     _check(load().aifmm_solve(ctypes.c_void_p(ptr), int(nrhs)))
 
 
@@ -170,7 +193,7 @@ def get_ranks(level: int, d: int, which: int = 0):
 
 
 def stats() -> dict:
-    out = np.zeros(16, dtype=np.float64)
+    out = np.zeros(len(STAT_NAMES), dtype=np.float64)
     _check(load().aifmm_stats(_ptr(out)))
     return dict(zip(STAT_NAMES, out.tolist()))
 
@@ -184,12 +207,15 @@ def set_timing(on: bool):
 
 
 def set_stream(stream_ptr: int):
+    global _bound_stream
     _check(load().aifmm_set_stream(ctypes.c_void_p(stream_ptr)))
+    _bound_stream = stream_ptr
 
 
 def debug_inverse(M):
     """In-place GPU inverse of a square CUDA float64 tensor (test hook); returns the inverse."""
     import torch
+    _bind_stream()
     Mc = M.to(torch.float64).t().contiguous()   # column-major storage of M
     _check(load().aifmm_debug_inverse(ctypes.c_void_p(Mc.data_ptr()), Mc.shape[0], Mc.shape[0]))
     return Mc.t()
@@ -200,6 +226,7 @@ def debug_tri_root(A):
     tensor (test hook; R unique up to row signs).  Returns (batch, m, min(n, m))."""
     import torch
     b, n, m = A.shape
+    _bind_stream()
     Ac = A.to(torch.float64).transpose(1, 2).contiguous()   # column-major storage per matrix
     r = min(n, m)
     M = torch.empty((b, r, m), dtype=torch.float64, device=A.device)
@@ -207,8 +234,27 @@ def debug_tri_root(A):
     return M.transpose(1, 2)
 
 
+def residual(X, B, rows=None) -> float:
+    """||A X - B||_F / ||B||_F over `rows` (user indices; all rows if None) by exact direct sum on
+    the GPU (row a9, verification).  X, B: torch.cuda float64 (N,) or (N, nrhs), user order."""
+    import torch
+    _bind_stream()
+    Xm = X[:, None] if X.dim() == 1 else X
+    Bm = B[:, None] if B.dim() == 1 else B
+    if Xm.shape != Bm.shape:
+        raise ValueError("X and B shapes differ")
+    Xf = Xm.to(torch.float64).t().contiguous()
+    Bf = Bm.to(torch.float64).t().contiguous()
+    r = None if rows is None else np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    out = ctypes.c_double(0.0)
+    _check(load().aifmm_residual(ctypes.c_void_p(Xf.data_ptr()), ctypes.c_void_p(Bf.data_ptr()), int(Xf.shape[0]),
+                                 None if r is None else _ptr(r), 0 if r is None else int(r.size), ctypes.byref(out)))
+    return out.value
+
+
 def matvec_build(tol: float):
     """Second NNCA at the matvec tolerance (row a8); requires build()."""
+    _bind_stream()
     _check(load().aifmm_matvec_build(float(tol)))
 
 
@@ -217,6 +263,7 @@ def matvec(X):
     import torch
     one = X.dim() == 1
     Xm = X[:, None] if one else X
+    _bind_stream()
     Xf = Xm.to(torch.float64).t().contiguous()      # (nrhs, N) row-major == N x nrhs column-major
     Yf = torch.empty_like(Xf)
     _check(load().aifmm_matvec(ctypes.c_void_p(Xf.data_ptr()), ctypes.c_void_p(Yf.data_ptr()), int(Xf.shape[0])))
@@ -228,7 +275,10 @@ def gmres(b, restart: int = 30, rtol: float = 1e-10, maxit: int = 1000, precond:
     """GMRES(restart) with the H2 matvec and (optionally) the AIFMM factor as right
     preconditioner; b: torch.cuda float64 (N,).  Returns (x, iterations, relative residual)."""
     import torch
-    bc = b.contiguous()
+    if not (isinstance(b, torch.Tensor) and b.is_cuda and b.dim() == 1):
+        raise TypeError("b must be a 1-D CUDA tensor")
+    _bind_stream()
+    bc = b.to(torch.float64).contiguous()
     x = torch.empty_like(bc)
     it = ctypes.c_int(0)
     rr = ctypes.c_double(0.0)

@@ -67,6 +67,8 @@ void gm_givens(double* H, int ldh, double* cs, double* sn, double* g, int j, dou
 void gm_backsub(const double* H, int ldh, const double* g, double* y, int k, cudaStream_t s);
 void gm_gemv(const double* V, long long ldv, const double* y, int k, long long n, double* out, cudaStream_t s);
 void set_scalar(double* dst, const double* src, double value, cudaStream_t s);
+void resid_finish(const double* part, int nchunks, long long nrows, int nrhs, const double* B, long long ldb,
+                  const int* rows_user, double* out, cudaStream_t s);
 
 // small integer kernels
 __global__ void iota_kernel(int* dst, long long n, int base) {
@@ -190,6 +192,7 @@ struct FLevel {
 
 struct Ctx {
   cudaStream_t s = nullptr;
+  bool inited = false;       // stream, uploader and flag allocated (s may legitimately be 0)
   bool own_stream = false;
   Uploader up;
   // persist: build outputs and the factor records the solve replays (pivot inverses, near-block
@@ -224,6 +227,11 @@ struct Ctx {
   FlopCounter fc_all, fc_schur;
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  // per-phase device time (CUDA events bracketing the phase's launches on c.s) and algorithmic
+  // work, for the bench's roofline entries: PH_PIVOT pivot factorisations, PH_TRI Householder
+  // first stage of the RRQR, PH_PQR truncated pivoted QR, PH_REDIR redirection GEMMs
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evp[4];
+  FlopCounter fcp[4];
   // accessors
   bool nonempty(int l, int b) const { return off[l][b + 1] > off[l][b]; }
   int count(int l, int b) const { return (int)(off[l][b + 1] - off[l][b]); }
@@ -247,11 +255,30 @@ struct Ctx {
 
 static Ctx* g_ctx = nullptr;
 static std::string g_err;
+enum { PH_PIVOT = 0, PH_TRI = 1, PH_PQR = 2, PH_REDIR = 3 };
+// records an event pair around a phase's launches when timing is on
+struct PhaseTimer {
+  Ctx& c;
+  int ph;
+  cudaEvent_t e0 = nullptr;
+  PhaseTimer(Ctx& c_, int ph_) : c(c_), ph(ph_) {
+    if (!c.timing) return;
+    AIFMM_CUDA(cudaEventCreate(&e0));
+    AIFMM_CUDA(cudaEventRecord(e0, c.s));
+  }
+  ~PhaseTimer() {
+    if (!e0) return;
+    cudaEvent_t e1 = nullptr;
+    if (cudaEventCreate(&e1) == cudaSuccess && cudaEventRecord(e1, c.s) == cudaSuccess) c.evp[ph].push_back({e0, e1});
+  }
+};
 
 static Ctx& ctx() {
   if (!g_ctx) g_ctx = new Ctx();
-  if (!g_ctx->s) {
-    AIFMM_CUDA(cudaStreamCreateWithFlags(&g_ctx->s, cudaStreamNonBlocking));
+  if (!g_ctx->inited) {
+    // a blocking stream: it is ordered after work on the legacy default stream (torch's default)
+    AIFMM_CUDA(cudaStreamCreate(&g_ctx->s));
+    g_ctx->inited = true;
     g_ctx->own_stream = true;
     g_ctx->up.init(g_ctx->s);
     g_before_launch = [] {
@@ -434,7 +461,13 @@ static void build_nnca(Ctx& c, std::vector<NLevel>& nnv, double eps, DevPool& po
         }
       }
     }
-    int* dfr = fr.empty() ? nullptr : c.up.put(fr);
+    // far ranges in level-lifetime device memory (not the staging arena: the chunk loop below
+    // synchronises, which rewinds the arena while later chunks still read the ranges)
+    int* dfr = nullptr;
+    if (!fr.empty()) {
+      dfr = pool.i(fr.size());
+      AIFMM_CUDA(cudaMemcpyAsync(dfr, fr.data(), sizeof(int) * fr.size(), cudaMemcpyHostToDevice, c.s));
+    }
     // ACA in chunks bounded by workspace
     int* drank = pool.i(nb);
     AIFMM_CUDA(cudaMemsetAsync(drank, 0, sizeof(int) * nb, c.s));
@@ -1035,7 +1068,15 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     if (!sym) tr.push_back(TriRootReq{sv[a].WT, nu, nu, m, sv[a].M, m});
   }
   g_expose.set("cmp.tri");
-  batched_tri_root(tr, c.work, c.up, c.s, &c.fc_all);
+  {
+    PhaseTimer pt(c, PH_TRI);
+    FlopCounter fp;
+    batched_tri_root(tr, c.work, c.up, c.s, &fp);
+    c.fc_all.flops += fp.flops;
+    c.fcp[PH_TRI].flops += fp.flops;
+    // algorithmic: read each candidate matrix once, write its triangular root once
+    for (const TriRootReq& q : tr) c.fcp[PH_TRI].bytes += 8.0 * ((double)q.n * q.m + (double)q.m * std::min(q.n, q.m));
+  }
   g_expose.set("cmp.pqr");
   if (g_prof.on) { g_prof.end("cmp.proj+triroot"); g_prof.begin(c.s); }
   struct SideW { double* W; int nc; };
@@ -1056,7 +1097,13 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
       pq.push_back(PqrTask{wv[a].W, f.V[b], m, m, m, wv[a].nc, k, 0, m - k, 0, dnorm + 2 * a + 1, c.tol_c, dt + 4 * a + 2, dt + 4 * a + 3});
     smem = std::max(smem, (size_t)std::max(wu[a].nc, wv[a].nc) + m + m);
   }
-  if (!pq.empty()) run_pqr(pq, c.up, c.s);
+  if (!pq.empty()) {
+    PhaseTimer pt(c, PH_PQR);
+    run_pqr(pq, c.up, c.s);
+    // algorithmic: read each m x r candidate matrix once and write the new basis columns (the
+    // number taken is decided on the device; counted as the read only)
+    for (const PqrTask& t : pq) c.fcp[PH_PQR].bytes += 8.0 * (double)t.m * t.ncols;
+  }
   std::vector<int> th = d2h(c, dt, 4 * na);
   g_expose.set("cmp.post");
   if (g_prof.on) { g_prof.end("cmp.pqrA"); g_prof.begin(c.s); }
@@ -1253,7 +1300,14 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
       cb.fill(F.p, F.ld, live(f, x), live(f, y), 0.0);
     }
   g_prof.hlap("cmp.redirect");
-  g.run(c.up, c.s, &c.fc_all);
+  {
+    PhaseTimer pt(c, PH_REDIR);
+    FlopCounter fp;
+    g.run(c.up, c.s, &fp);
+    c.fc_all.flops += fp.flops;
+    c.fcp[PH_REDIR].flops += fp.flops;
+    c.fcp[PH_REDIR].bytes += fp.bytes;
+  }
   cb.run(c.up, c.s);
   for (auto& pr : S) f.pending.erase(pr);
   if (g_prof.on) g_prof.end("cmp.redirect");
@@ -1380,7 +1434,14 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     inv.push_back(InvReq{r.G, n, n, f.dinfo + i});
   }
   cb.run(c.up, c.s);
-  batched_inverse(inv, c.work, c.up, c.s, &c.fc_all);
+  {
+    PhaseTimer pt(c, PH_PIVOT);
+    FlopCounter fp;
+    batched_inverse(inv, c.work, c.up, c.s, &fp);
+    c.fc_all.flops += fp.flops;
+    c.fcp[PH_PIVOT].flops += fp.flops;
+    for (const InvReq& r : inv) c.fcp[PH_PIVOT].bytes += 16.0 * r.n * r.n;   // read + write each pivot once
+  }
   static const bool dbg_g11 = getenv("AIFMM_DEBUG_G11") != nullptr;   // debug: |G11| of full boxes (R28)
   if (dbg_g11) {
     for (int i : cs) {
@@ -1963,6 +2024,57 @@ static void gmres_dev(Ctx& c, const double* b, double* x, int restart, double rt
   *relres = beta / bnorm;
 }
 
+// ------------------------------------------------------------------------------------ residual
+// Row a9 (verification, not timed): ||A X - B||_F / ||B||_F over the sampled rows by exact direct
+// sum (A_ij = K(x_i, x_j), A_ii = diag).  X, B: device, user order, n x nrhs
+// column-major.  The rows are split into blocks of 128 (one thread per row) and the sources
+// into chunks; each (row block, chunk) pair writes its own partial product (kmv_kernel), and
+// the partials are summed in chunk order (deterministic).
+static double residual_dev(Ctx& c, const double* X, const double* B, int nrhs, const int64_t* rows, long long nrows) {
+  const long long n = c.n;
+  c.work.reset();
+  std::vector<int> permh = d2h(c, c.perm, (size_t)n);
+  std::vector<int> inv((size_t)n);
+  for (long long j = 0; j < n; ++j) inv[permh[j]] = (int)j;
+  std::vector<int> rt((size_t)nrows), ru((size_t)nrows);
+  for (long long i = 0; i < nrows; ++i) {
+    const long long u = rows ? rows[i] : i;
+    AIFMM_REQUIRE(u >= 0 && u < n, AIFMM_EINVALID_ARG, "residual row out of range");
+    ru[i] = (int)u;
+    rt[i] = inv[u];
+  }
+  int* drt = c.work.i(nrows);
+  int* dru = c.work.i(nrows);
+  AIFMM_CUDA(cudaMemcpyAsync(drt, rt.data(), sizeof(int) * nrows, cudaMemcpyHostToDevice, c.s));
+  AIFMM_CUDA(cudaMemcpyAsync(dru, ru.data(), sizeof(int) * nrows, cudaMemcpyHostToDevice, c.s));
+  double* Xt = c.work.d((size_t)n * nrhs);
+  LAUNCH(permute_rows_kernel, gsz(n * nrhs), 256, 0, c.s, X, Xt, c.perm, n, nrhs, 0);
+  const long long nblk = (nrows + 127) / 128;
+  const int S = (int)std::max<long long>(1, std::min<long long>(std::max<long long>(1, 2048 / nblk), (n + 1023) / 1024));
+  const long long cs = (n + S - 1) / S;
+  double* part = c.work.d((size_t)S * nrows * nrhs);
+  std::vector<KmvTarget> tg;
+  std::vector<KmvSource> src;
+  for (int s = 0; s < S; ++s) {
+    const long long c0 = s * cs, nc = std::max<long long>(0, std::min(cs, n - c0));
+    src.push_back(KmvSource{nullptr, (int)c0, (int)nc, Xt + c0, (int)n, 0});
+  }
+  for (long long rb = 0; rb < nblk; ++rb)
+    for (int s = 0; s < S; ++s) {
+      const long long r0 = rb * 128;
+      tg.push_back(KmvTarget{drt + r0, 0, (int)std::min<long long>(128, nrows - r0), part + (size_t)s * nrows * nrhs + r0,
+                             (int)nrows, s, s + 1});
+    }
+  const KmvTarget* dtg = c.up.put(tg);
+  const KmvSource* dsrc = c.up.put(src);
+  launch_kmv(dtg, dsrc, (int)tg.size(), c.pts, c.kp, nrhs, 0, c.s);
+  double* dout = c.work.d(2);
+  resid_finish(part, S, nrows, nrhs, B, n, dru, dout, c.s);
+  std::vector<double> o = d2h(c, dout, 2);
+  c.work.reset();
+  return o[1] > 0.0 ? std::sqrt(o[0] / o[1]) : std::sqrt(o[0]);
+}
+
 }  // namespace aifmm
 
 // ====================================================================================== C-ABI
@@ -2052,6 +2164,10 @@ int aifmm_factor(void) {
   c.symmetric = getenv("AIFMM_ASYMMETRIC") == nullptr;   // R27 (debug toggle: independent U/V sides)
   for (auto& e : c.ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   c.ev.clear();
+  for (auto& v : c.evp) {
+    for (auto& e : v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    v.clear();
+  }
   factor_all(c);
   c.up.sync();
   double sch = 0.0;
@@ -2063,6 +2179,20 @@ int aifmm_factor(void) {
     cudaEventDestroy(e.second);
   }
   c.ev.clear();
+  for (int ph = 0; ph < 4; ++ph) {
+    double t = 0.0;
+    for (auto& e : c.evp[ph]) {
+      float ms = 0.f;
+      AIFMM_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+      t += ms;
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    c.evp[ph].clear();
+    c.stats[AIFMM_STAT_PIVOT_MS + 3 * ph] += t;
+    c.stats[AIFMM_STAT_PIVOT_FLOPS + 3 * ph] = c.fcp[ph].flops;
+    c.stats[AIFMM_STAT_PIVOT_BYTES + 3 * ph] = c.fcp[ph].bytes;
+  }
   c.stats[AIFMM_STAT_SCHUR_MS] += sch;
   c.stats[AIFMM_STAT_SCHUR_FLOPS] = c.fc_schur.flops;
   c.stats[AIFMM_STAT_SCHUR_BYTES] = c.fc_schur.bytes;
@@ -2113,7 +2243,7 @@ int aifmm_solve_host(double* B, int nrhs) {
 void aifmm_free(void) {
   if (!g_ctx) return;
   Ctx& c = *g_ctx;
-  if (c.s) cudaStreamSynchronize(c.s);
+  if (c.inited) cudaStreamSynchronize(c.s);
   c.fl.clear();
   c.nn.clear();
   c.hnn.clear();
@@ -2136,12 +2266,13 @@ const char* aifmm_last_error(void) { return g_err.c_str(); }
 int aifmm_set_stream(void* stream) {
   CAPI_BEGIN
   Ctx& c = ctx();
+  cudaStream_t ns = static_cast<cudaStream_t>(stream);
+  if (ns == c.s) return 0;
+  c.up.set_stream(ns);               // flushes and completes everything queued on the old stream
   AIFMM_CUDA(cudaStreamSynchronize(c.s));
   if (c.own_stream) cudaStreamDestroy(c.s);
-  c.s = static_cast<cudaStream_t>(stream);
+  c.s = ns;
   c.own_stream = false;
-  c.up.free_all();
-  c.up.init(c.s);
   CAPI_END
 }
 
@@ -2221,6 +2352,8 @@ int aifmm_reset_counters(void) {
   c.up.syncs = 0;
   c.fc_all = FlopCounter{};
   c.fc_schur = FlopCounter{};
+  for (auto& f : c.fcp) f = FlopCounter{};
+  for (int i = AIFMM_STAT_PIVOT_MS; i < AIFMM_NSTATS; ++i) c.stats[i] = 0;
   c.stats[AIFMM_STAT_SCHUR_MS] = 0;
   c.stats[AIFMM_STAT_SCHUR_LAUNCHES] = 0;
   c.stats[AIFMM_STAT_COMPRESSIONS] = 0;
@@ -2288,6 +2421,17 @@ int aifmm_gmres(const double* b, double* x, int restart, double rtol, int maxit,
   LAUNCH(finite_kernel, gsz(c.n), 256, 0, c.s, b, c.n, c.dflag);
   check_flag(c, AIFMM_ENONFINITE, "non-finite right-hand side");
   gmres_dev(c, b, x, restart, rtol, maxit, precond, iters, relres);
+  CAPI_END
+}
+
+int aifmm_residual(const double* X, const double* B, int nrhs, const int64_t* rows, int64_t nrows, double* rel) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built, AIFMM_ESTATE, "residual before build");
+  AIFMM_REQUIRE(X && B && rel && nrhs >= 1, AIFMM_EINVALID_ARG, "residual: null pointer or nrhs < 1");
+  const long long nr = rows ? (long long)nrows : c.n;
+  AIFMM_REQUIRE(nr >= 1, AIFMM_EINVALID_ARG, "residual: no rows");
+  *rel = residual_dev(c, X, B, nrhs, rows, nr);
   CAPI_END
 }
 

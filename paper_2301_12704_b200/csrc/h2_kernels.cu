@@ -188,6 +188,42 @@ __global__ void set_scalar_kernel(double* dst, const double* src, double value) 
   if (threadIdx.x == 0) *dst = src ? *src : value;
 }
 
+// Direct-sum residual (verification only): part[s] holds the partial
+// products A(rows, chunk_s) X of source chunk s (kmv_kernel); this sums them in chunk order and
+// accumulates sum (y - b)^2 and sum b^2 over the sampled rows in a fixed order (one CTA).
+constexpr int RES_NT = 1024;
+__global__ void __launch_bounds__(RES_NT) resid_finish_kernel(const double* __restrict__ part, int nchunks, long long nrows,
+                                                              int nrhs, const double* __restrict__ B, long long ldb,
+                                                              const int* __restrict__ rows_user, double* __restrict__ out) {
+  __shared__ double r1[RES_NT / 32], r2[RES_NT / 32];
+  double a = 0.0, bb = 0.0;
+  const long long tot = nrows * nrhs;
+  for (long long e = threadIdx.x; e < tot; e += RES_NT) {
+    const long long i = e % nrows, c = e / nrows;
+    double y = 0.0;
+    for (int s = 0; s < nchunks; ++s) y += part[(size_t)s * tot + e];
+    const double b = B[(size_t)c * ldb + rows_user[i]];
+    a += (y - b) * (y - b);
+    bb += b * b;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    bb += __shfl_xor_sync(0xffffffffu, bb, o);
+  }
+  if ((threadIdx.x & 31) == 0) { r1[threadIdx.x >> 5] = a; r2[threadIdx.x >> 5] = bb; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t1 = 0.0, t2 = 0.0;
+    for (int w = 0; w < RES_NT / 32; ++w) { t1 += r1[w]; t2 += r2[w]; }
+    out[0] = t1;
+    out[1] = t2;
+  }
+}
+void resid_finish(const double* part, int nchunks, long long nrows, int nrhs, const double* B, long long ldb,
+                  const int* rows_user, double* out, cudaStream_t s) {
+  LAUNCH(resid_finish_kernel, 1, RES_NT, 0, s, part, nchunks, nrows, nrhs, B, ldb, rows_user, out);
+}
+
 static int vgrid(long long n) { return (int)std::min<long long>(std::max<long long>((n + VEC_NT - 1) / VEC_NT, 1), 148 * 8); }
 void vec_dot(const double* a, const double* b, long long n, double* part, double* out, int sqrt_mode, cudaStream_t s) {
   LAUNCH(dot_partial_kernel, DOT_BLOCKS, VEC_NT, 0, s, a, b, n, part);

@@ -250,14 +250,23 @@ class DevPool {
   size_t used_ = 0, held_ = 0;
 };
 
-// Pinned host staging + device mirror for task arrays.  An append is copied H2D at once;
-// the region is reused only after sync() (stream synchronised).
+// Pinned host staging + device mirror for task arrays.  Appends are copied H2D by the next
+// flush(); the region is reused only after sync() (stream synchronised), which bumps gen():
+// a device pointer returned by put() is valid only while gen() is unchanged, so a caller that
+// keeps one across calls that may sync (reserve / put / GemmBatch::run) must re-put its data
+// when gen() moved (see batched_inverse, batched_tri_root).
 class Uploader {
  public:
   void init(cudaStream_t s, size_t cap = (size_t)256 << 20) {
     s_ = s;
     grow(cap);
   }
+  // switch to another stream: everything staged so far is flushed and completed on the old one
+  void set_stream(cudaStream_t s) {
+    if (h_) sync();
+    s_ = s;
+  }
+  unsigned long long gen() const { return gen_; }
   ~Uploader() { free_all(); }
   void free_all() {
     if (h_) cudaFreeHost(h_);
@@ -302,6 +311,7 @@ class Uploader {
     AIFMM_CUDA(cudaStreamSynchronize(s_));
     used_ = flushed_ = 0;
     ++syncs;
+    ++gen_;
     g_expose.synced();
   }
   long long syncs = 0;
@@ -313,7 +323,9 @@ class Uploader {
     AIFMM_CUDA(cudaMalloc(&d_, cap));
     cap_ = cap;
     used_ = flushed_ = 0;
+    ++gen_;
   }
+  unsigned long long gen_ = 0;
   cudaStream_t s_ = 0;
   char* h_ = nullptr;
   char* d_ = nullptr;
@@ -549,10 +561,12 @@ inline void batched_inverse(const std::vector<InvReq>& reqs, Pool& work, Uploade
     nmax = std::max(nmax, r.n);
   }
   const void* dt = up.put(tb.data(), tb.size());
+  unsigned long long dgen = up.gen();
   // few matrices: 8-CTA clusters per matrix (row slices in shared memory); many: one CTA each
   static const bool gj_single = getenv("AIFMM_GJ_SINGLE") != nullptr;   // debug toggle
   const bool cluster = !gj_single && (int)big.size() <= 148 && nmax <= 8 * 700;
   for (int j = 0; j < nmax; j += GJ_PANEL) {
+    if (up.gen() != dgen) { dt = up.put(tb.data(), tb.size()); dgen = up.gen(); }   // staging rewound
     if (cluster) launch_gj_panel_cluster(dt, (int)big.size(), j, nmax, s);
     else launch_gj_panel(dt, (int)big.size(), j, s);
     GemmBatch g;
@@ -571,6 +585,7 @@ inline void batched_inverse(const std::vector<InvReq>& reqs, Pool& work, Uploade
     }
     g.run(up, s);
   }
+  if (up.gen() != dgen) dt = up.put(tb.data(), tb.size());
   launch_gj_unscramble(dt, (int)big.size(), nmax, s);
 }
 
@@ -680,9 +695,19 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   const void* dt = up.put(tb.data(), tb.size());
   double* const* douts = up.put(outs);
   const int* dldo = up.put(ldo);
+  unsigned long long dgen = up.gen();
+  auto restage = [&] {   // the staging arena was rewound by a sync: upload the descriptors again
+    if (up.gen() == dgen) return;
+    up.reserve(tb.size() + outs.size() * 8 + ldo.size() * 4 + 1024);
+    dt = up.put(tb.data(), tb.size());
+    douts = up.put(outs);
+    dldo = up.put(ldo);
+    dgen = up.gen();
+  };
   if (g_prof.on) { g_prof.end("cmp.proj"); g_prof.begin(s); }
   for (int j = 0; j < rmax; j += HH_PANEL) {
     if (g_prof.on) g_prof.begin(s);
+    restage();
     const char* d0 = static_cast<const char*>(dt);
     const size_t o1 = nrg, o2 = o1 + nsm, o3 = o2 + nsmall, o4 = o3 + nrc, o5 = o4 + nmid;
     if (nrg && j < nmax_rg) launch_hh_panel(d0, (int)nrg, j, s, 4, nmax_rg);
@@ -702,10 +727,16 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
       for (int n0 = 0; n0 < nc; n0 += 64) ut.push_back(make_int2((int)i, n0));
     }
     if (g_prof.on) { g_prof.end("hh.panel"); g_prof.begin(s); }
-    if (!ut.empty()) launch_hh_update(dt, up.put(ut), (int)ut.size(), j, s);
+    if (!ut.empty()) {
+      up.reserve(tb.size() + outs.size() * 8 + ldo.size() * 4 + ut.size() * sizeof(int2) + 2048);
+      restage();
+      const int2* dut = up.put(ut);
+      launch_hh_update(dt, dut, (int)ut.size(), j, s);
+    }
     if (g_prof.on) g_prof.end("hh.trail");
   }
   if (g_prof.on) g_prof.begin(s);
+  restage();
   launch_hh_extract(dt, (int)reqs.size(), douts, dldo, s);
   if (!stacks.empty()) batched_tri_root(stacks, work, up, s, fc, tsqr_m);   // next TSQR round
 }

@@ -182,3 +182,25 @@ def test_config2_full_size_parity():
     g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg2_oracle_rounding_sensitivity.json")))
     sens = g.get("rel_solution_diff_max", g["rel_solution_diff_inv_vs_lu_solve"])
     assert rel <= max(10 * cfg.tol, 3 * sens), (rel, sens)
+
+
+def test_gpu_residual_matches_oracle_direct_sum():
+    """Row a9 on the GPU (aifmm_residual): the direct-sum relative residual of a solution equals
+    the oracle's (oracle/dense.py: residual) on all rows and on a sampled row set, for every
+    kernel (several 128-row blocks, a ragged last block, several source chunks)."""
+    for kid, kp, d, kind in ((0, (10.0, 0.0), 2, "uniform_pm1"), (1, (1.01, 0.1), 2, "uniform_pm1"),
+                             (2, (100.0, 0.0), 3, "uniform_01")):
+        pts, b = W.small_problem(d=d, n=2900, kind=kind, seed=40 + kid, nrhs=3)
+        G.free()
+        G.build(torch.from_numpy(pts).cuda(), kid, kp, 40, 1e-6)
+        G.factor()
+        X = G.solve(torch.from_numpy(b).cuda())
+        x = X.cpu().numpy()
+        rows = np.sort(np.random.default_rng(kid).choice(2900, 700, replace=False))
+        for rr in (None, rows):
+            ro = dense.residual(pts, kid, kp, x, b, rr)
+            rg = G.residual(X, torch.from_numpy(b).cuda(), rr)
+            assert abs(rg - ro) <= 1e-9 * ro + 1e-15, (kid, rg, ro)
+        # an exact solution of a perturbed system: residual of (X, A X) is ~0
+        Y = torch.from_numpy(dense.dense_matrix(pts, kid, kp) @ x).cuda()
+        assert G.residual(X, Y) <= 1e-13
