@@ -64,6 +64,15 @@ int aifmm_build(const double* points, int64_t n, int d, int kernel_id,
  * redirection; used by the tests to separate NNCA error from compression error). */
 int aifmm_set_compression_tol(double tol_c);
 
+/* aifmm_set_algorithm — optional, before aifmm_factor (default 3, kept across builds):
+ *   3  Algorithm 3: far fill-ins accumulated and compressed / redirected once,
+ *      just before one of their boxes is eliminated (the paper's efficient variant);
+ *   2  Algorithm 2: fill-ins compressed as soon as they are created or updated,
+ *      here right after the colour whose eliminations created them (the
+ *      ablation of P:1090-1096).  Same results up to O(tol); more compressions.
+ * Errors: EINVALID_ARG. */
+int aifmm_set_algorithm(int alg);
+
 /* aifmm_factor — elimination with colour-batched Algorithm 3 (T_Af).
  * Needs a successful build.  Errors: ESTATE, ESINGULAR_PIVOT, ECUDA, EOOM. */
 int aifmm_factor(void);
@@ -112,8 +121,11 @@ int aifmm_get_ranks(int level, int which, int32_t* ranks);
  *   X is read, Y is overwritten; they must not alias.  Near field and M2L kernel entries are
  *   evaluated on the fly (never stored).  AIFMM_ESTATE before aifmm_matvec_build.
  * aifmm_gmres — solve A x = b by restarted GMRES(restart) (modified Gram-Schmidt, Givens),
- *   matrix = the H2 matvec, right preconditioner = the AIFMM factorization (aifmm_solve) when
- *   precond != 0 (requires aifmm_factor), stopping when ||b - A x|| / ||b|| <= rtol (Arnoldi
+ *   matrix = the H2 matvec, right preconditioner: precond = 1 the AIFMM factorization
+ *   (aifmm_solve; requires aifmm_factor), precond = 2 the leaf block-diagonal inverse
+ *   blockdiag(A(points(b), points(b)))^-1 (the paper's block-diagonal comparison, P:1628-1629,
+ *   table; blocks evaluated exactly and inverted on the first use), precond = 0
+ *   none; stopping when ||b - A x|| / ||b|| <= rtol (Arnoldi
  *   estimate inside a cycle, true residual at each restart) or after maxit iterations.
  *   b (read) and x (written): device, N doubles, user order.  iters / relres: host out.
  *   AIFMM_ENONFINITE for a non-finite b. */

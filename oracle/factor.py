@@ -24,8 +24,8 @@ start of each level by an exact change of variables (the update derivations assu
 U~^* U~ = I); R14 project-then-compress RRQR with truncation
 tol_c * ||F||_F and Galerkin redirection A <- U~^*(U A V^* + F) V~, which with orthonormal
 bases equals L A R^* + R~^* and zero-pads the other
-M2L, M2M, L2L blocks; R15 equal box ranks |z_i| = |y_i| (needed for a square
-pivot [[K, U],[V^*, 0]]) by extending the shorter side's pivoted QR, capped at m_i;
+M2L, M2M, L2L blocks; R15 + R27 equal box ranks |z_i| = |y_i| (needed for a
+square pivot [[K, U],[V^*, 0]]): one-sided compression, V's new columns = U's, capped at m_i;
 R16 pivot inverse G = P_i^{-1} by LU with partial pivoting; R17 (Z_i, y_i) = -G22;
 R8b the RRQR runs on the triangular factor of the projected candidate matrix (tri_root).
 """
@@ -57,20 +57,6 @@ def tri_root(W):
     return np.ascontiguousarray(R.T)
 
 
-def extend_basis(W, B, tau, t):
-    """R15: exactly t new orthonormal directions: pivoted QR of W (continued past its
-    truncation point if needed), then projected identity columns if W is exhausted."""
-    Q, _ = pivoted_qr_extend(W, B, tau, t, t)
-    if Q.shape[1] < t:
-        BB = np.concatenate([B, Q], axis=1)
-        m = W.shape[0]
-        WI = np.eye(m) - BB @ BB.T
-        WI = WI - BB @ (BB.T @ WI)
-        Q2, _ = pivoted_qr_extend(WI, BB, 0.0, t - Q.shape[1], t - Q.shape[1])
-        Q = np.concatenate([Q, Q2], axis=1)
-    return Q
-
-
 class Level:
     pass
 
@@ -78,13 +64,15 @@ class Level:
 class AIFMM:
     """Oracle AIFMM: build (tree, lists, colours, NNCA), factor, solve."""
 
-    def __init__(self, points, kernel_id, kparams, leaf_size, tol, tol_c=None, nnca_eps=None, symmetric=True):
+    def __init__(self, points, kernel_id, kparams, leaf_size, tol, tol_c=None, nnca_eps=None, algorithm=3):
         self.kid, self.kp = kernel_id, tuple(kparams)
-        # reading R27: every kernel here is symmetric (A_ij = A_ji, targets = sources, P:1248), so
-        # the column-side fill-ins are the transposes of the row-side ones (F_pb^T = F_bp) and
-        # the V-side basis extension equals the U-side one in exact arithmetic; computing it
-        # once keeps V_b = U_b exactly (symmetric pivots [[K, U], [U^T, 0]]).
-        self.symmetric = symmetric
+        # algorithm = 3: Alg. 3 (P:1107-1164), far fill-ins compressed once, just before one of
+        # their members is eliminated; algorithm = 2: Alg. 2 (P:731-791), compressed as soon as
+        # they are created or updated -- here right after the colour that created them (SURVEY
+        # §8(f) row f2, reading R29)
+        if algorithm not in (2, 3):
+            raise ValueError("algorithm must be 2 or 3")
+        self.algorithm = algorithm
         self.tol = tol
         self.tol_c = tol if tol_c is None else tol_c
         self.tree = Tree(points, leaf_size)
@@ -189,29 +177,22 @@ class AIFMM:
             part.setdefault(a, []).append(b)
             part.setdefault(b, []).append(a)
         affected = sorted(b for b in part if not lv.E[b])
-        newU, newV = {}, {}
+        newU = {}
         for b in affected:
             ps = sorted(part[b])
             m, k = lv.m[b], lv.k[b]
+            # reading R27: every kernel here is symmetric (A_ij = A_ji, targets = sources),
+            # so the column-side fill-ins are the transposes of the row-side ones (F_pb^T = F_bp)
+            # and the V-side basis extension of P:852-863 equals the U-side one in exact
+            # arithmetic: it is computed once, from row X_b, and V_b's new columns are U_b's (the
+            # pivots stay [[K, U], [U^T, 0]], square: |z_b| = |y_b| as P:753 needs, R15)
             FU = np.concatenate([lv.F[(b, q)] for q in ps], axis=1)       # row X_b
             nU = np.linalg.norm(FU)
             WU = tri_root(FU - lv.U[b] @ (lv.U[b].T @ FU))
-            cap = m - k
-            _, tU = pivoted_qr_extend(WU, lv.U[b], self.tol_c * nU, 0, cap)
-            if self.symmetric:                                              # R27
-                tt = tU
-                QU = extend_basis(WU, lv.U[b], self.tol_c * nU, tt)
-                QV = QU
-            else:
-                FV = np.concatenate([lv.F[(p, b)].T for p in ps], axis=1)     # column x_b
-                nV = np.linalg.norm(FV)
-                WV = tri_root(FV - lv.V[b] @ (lv.V[b].T @ FV))
-                _, tV = pivoted_qr_extend(WV, lv.V[b], self.tol_c * nV, 0, cap)
-                tt = max(tU, tV)
-                QU = extend_basis(WU, lv.U[b], self.tol_c * nU, tt)
-                QV = extend_basis(WV, lv.V[b], self.tol_c * nV, tt)
+            # R8 with tmin = 0: the columns taken are exactly the t_trunc of the truncation test
+            QU, tt = pivoted_qr_extend(WU, lv.U[b], self.tol_c * nU, 0, m - k)
+            assert QU.shape[1] == tt
             newU[b] = np.concatenate([lv.U[b], QU], axis=1)
-            newV[b] = np.concatenate([lv.V[b], QV], axis=1)
             self.stats["compressions"] += 1
             g = self.stats["rank_growth"].setdefault(l, 0)
             self.stats["rank_growth"][l] = g + tt
@@ -229,7 +210,7 @@ class AIFMM:
                 lv.A[(c, b)] = _pad(A, A.shape[0], k1)
             lv.k[b] = k1
         for b in affected:
-            lv.U[b], lv.V[b] = newU[b], newV[b]
+            lv.U[b], lv.V[b] = newU[b], newU[b].copy()
         # redirect the fill-ins (Galerkin projection onto the new bases)
         for (a, b) in S:
             for (x, y) in ((a, b), (b, a)):
@@ -304,6 +285,8 @@ class AIFMM:
                     self._eliminate(lv, i, skip_schur=i in full)
                 for i in cset:
                     lv.E[i] = True
+                if self.algorithm == 2 and lv.pending:       # Alg. 2: compress on creation
+                    self._compress(lv, sorted(lv.pending))
             assert not lv.pending and not lv.F, "pending far fill-ins at level end"
             self.stats["max_rank"][l] = max(lv.k.values())
             self.levels[l] = lv

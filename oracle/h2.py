@@ -141,3 +141,26 @@ def gmres(matvec, b, precond=None, restart=30, rtol=1e-10, maxit=1000):
         r = b - matvec(x)
         beta = np.linalg.norm(r)
     return x, it, float(beta / bnorm)
+
+
+def block_diagonal_precond(tree, kernel_id, kparams):
+    """The block-diagonal preconditioner of the paper's comparison (I_BD, table
+    P:1684-1700): M = blockdiag(A(points(b), points(b))) over the leaves b
+    of the tree, each block written out exactly (kernels.block) and inverted (numpy.linalg.inv).
+    Returns v -> M^{-1} v in user order."""
+    L = tree.L
+    blocks = []
+    for b in tree.nonempty(L):
+        a0, a1 = tree.point_range(L, b)
+        idx = np.arange(a0, a1)
+        blocks.append((a0, a1, np.linalg.inv(kernels.block(kernel_id, kparams, tree.points, idx, idx))))
+
+    def apply(v):
+        vs = np.asarray(v, dtype=np.float64)[tree.perm]
+        out = np.empty_like(vs)
+        for a0, a1, Binv in blocks:
+            out[a0:a1] = Binv @ vs[a0:a1]
+        res = np.empty_like(out)
+        res[tree.perm] = out
+        return res
+    return apply

@@ -23,7 +23,7 @@ SYMBOLS = ["aifmm_build", "aifmm_set_compression_tol", "aifmm_factor", "aifmm_so
            "aifmm_get_tree", "aifmm_get_level_offsets", "aifmm_get_lists", "aifmm_get_colours",
            "aifmm_get_ranks", "aifmm_stats", "aifmm_reset_counters", "aifmm_set_timing",
            "aifmm_debug_inverse", "aifmm_debug_tri_root", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres",
-           "aifmm_residual"]
+           "aifmm_residual", "aifmm_set_algorithm"]
 STAT_NAMES = ["build_ms", "factor_ms", "solve_ms", "levels", "top_size", "factor_flops",
               "schur_flops", "schur_ms", "launches", "compressions", "max_rank", "device_bytes",
               "schur_bytes", "schur_launches", "solve_bytes", "host_syncs",
@@ -70,6 +70,7 @@ def load(path: str = LIB_PATH):
     lib.aifmm_matvec.argtypes = [P, P, I]
     lib.aifmm_gmres.argtypes = [P, P, I, D, I, I, P, P]
     lib.aifmm_residual.argtypes = [P, P, I, P, I64, P]
+    lib.aifmm_set_algorithm.argtypes = [I]
     _lib = lib
     return lib
 
@@ -113,6 +114,11 @@ def build(points, kernel_id: int, kparams, leaf_size: int, tol: float):
 
 def set_compression_tol(tol_c: float):
     _check(load().aifmm_set_compression_tol(float(tol_c)))
+
+
+def set_algorithm(alg: int):
+    """3 = Algorithm 3 (deferred compression, default), 2 = Algorithm 2 (compress on creation)."""
+    _check(load().aifmm_set_algorithm(int(alg)))
 
 
 def factor():
@@ -271,9 +277,13 @@ def matvec(X):
     return Y[:, 0].contiguous() if one else Y.contiguous()
 
 
-def gmres(b, restart: int = 30, rtol: float = 1e-10, maxit: int = 1000, precond: bool = True):
-    """GMRES(restart) with the H2 matvec and (optionally) the AIFMM factor as right
-    preconditioner; b: torch.cuda float64 (N,).  Returns (x, iterations, relative residual)."""
+PRECOND = {False: 0, True: 1, None: 0, 0: 0, 1: 1, 2: 2, "none": 0, "aifmm": 1, "block_diagonal": 2}
+
+
+def gmres(b, restart: int = 30, rtol: float = 1e-10, maxit: int = 1000, precond=True):
+    """GMRES(restart) with the H2 matvec; right preconditioner: True / 1 / "aifmm" the AIFMM
+    factor, 2 / "block_diagonal" the leaf block-diagonal inverse, False / 0 / "none" none.
+    b: torch.cuda float64 (N,).  Returns (x, iterations, relative residual)."""
     import torch
     if not (isinstance(b, torch.Tensor) and b.is_cuda and b.dim() == 1):
         raise TypeError("b must be a 1-D CUDA tensor")
@@ -283,5 +293,5 @@ def gmres(b, restart: int = 30, rtol: float = 1e-10, maxit: int = 1000, precond:
     it = ctypes.c_int(0)
     rr = ctypes.c_double(0.0)
     _check(load().aifmm_gmres(ctypes.c_void_p(bc.data_ptr()), ctypes.c_void_p(x.data_ptr()), int(restart), float(rtol),
-                              int(maxit), 1 if precond else 0, ctypes.byref(it), ctypes.byref(rr)))
+                              int(maxit), PRECOND[precond], ctypes.byref(it), ctypes.byref(rr)))
     return x, it.value, rr.value

@@ -206,11 +206,17 @@ struct Ctx {
   bool h2_built = false;
   double h2_tol = 0;
   DevPool h2pool, h2work, gmpool;
+  // leaf block-diagonal inverses (GMRES precond 2, row f3)
+  DevPool bdpool;
+  bool bd_ready = false;
+  double* bdinv = nullptr;
+  std::vector<long long> bdoff;
   int d = 0, kid = 0, leaf = 0, L = 0;
   long long n = 0;
   KernelParams kp{};
   double tol = 0, tol_c = -1, tol_c_user = -1;
   bool symmetric = true;                   // reading R27: V-side bases reuse the U-side ones
+  int algorithm = 3;                       // 3: Alg. 3; 2: Alg. 2 (R29)
   double* pts = nullptr;                   // sorted points (device)
   int* perm = nullptr;                     // device int32
   int* dflag = nullptr;                    // device int error flag
@@ -1640,6 +1646,10 @@ static void factor_levels(Ctx& c) {
       g_prof.begin(c.s);
       eliminate_update(c, f, cs, plan);
       g_prof.end(("eliminate.L" + std::to_string(l)).c_str());
+      if (c.algorithm == 2 && !f.pending.empty()) {   // Alg. 2: compress on creation (R29)
+        std::vector<std::pair<int, int>> all(f.pending.begin(), f.pending.end());
+        compress(c, f, all, [] {});
+      }
     }
     AIFMM_REQUIRE(f.pending.empty(), AIFMM_ESINGULAR_PIVOT, "pending far fill-ins at level end");
     if (g_prof.on) {
@@ -1949,8 +1959,57 @@ static void matvec_dev(Ctx& c, const double* X, double* Y, int nrhs) {
   c.up.sync();
 }
 
+// Block-diagonal preconditioner (the paper's I_BD column, P:1628-1629,
+// table): M = blockdiag(A(points(b), points(b))) over the leaves b, each block
+// evaluated exactly and inverted once (batched Gauss-Jordan, R16); stored in c.bdpool.
+static void bd_prepare(Ctx& c) {
+  if (c.bd_ready) return;
+  const int L = c.L;
+  const int nb = 1 << (c.d * L);
+  c.bdpool.reset();
+  c.bdoff.assign(nb + 1, 0);
+  for (int b = 0; b < nb; ++b) c.bdoff[b + 1] = c.bdoff[b] + (long long)c.count(L, b) * c.count(L, b);
+  c.bdinv = c.bdpool.d(std::max<long long>(c.bdoff[nb], 1));
+  std::vector<KEvalTask> kt;
+  std::vector<InvReq> inv;
+  int* dinfo = c.bdpool.i(nb);
+  AIFMM_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int) * nb, c.s));
+  AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
+  for (int b = 0; b < nb; ++b) {
+    const int m = c.count(L, b);
+    if (!m) continue;
+    const int r0 = (int)c.off[L][b];
+    kt.push_back(KEvalTask{c.bdinv + c.bdoff[b], m, m, m, nullptr, nullptr, r0, r0});
+    inv.push_back(InvReq{c.bdinv + c.bdoff[b], m, m, dinfo + b});
+  }
+  if (!kt.empty()) launch_keval(c.up.put(kt), (int)kt.size(), 4, c.pts, c.kp, c.dflag, c.s);
+  batched_inverse(inv, c.work, c.up, c.s, &c.fc_all);
+  check_flag(c, AIFMM_ECOINCIDENT, "coincident points with a singular kernel");
+  std::vector<int> info = d2h(c, dinfo, nb);
+  for (int b = 0; b < nb; ++b)
+    if (info[b]) throw Error(AIFMM_ESINGULAR_PIVOT, "singular leaf block " + std::to_string(b));
+  c.work.reset();
+  c.bd_ready = true;
+}
+// v <- M^{-1} v (user order, one column): gather to tree order, one GEMM per leaf, scatter back
+static void bd_apply(Ctx& c, double* v, double* tmp) {
+  const int L = c.L;
+  const long long n = c.n;
+  LAUNCH(permute_rows_kernel, gsz(n), 256, 0, c.s, v, tmp, c.perm, n, 1, 0);
+  GemmBatch g;
+  for (int b = 0; b < (1 << (c.d * L)); ++b) {
+    const int m = c.count(L, b);
+    if (!m) continue;
+    g.task(tmp + n + c.off[L][b], m, m, 1, 0.0);
+    g.term(1.0, c.bdinv + c.bdoff[b], m, 0, tmp + c.off[L][b], m, 0, m);
+  }
+  g.run(c.up, c.s, &c.fc_all);
+  LAUNCH(permute_rows_kernel, gsz(n), 256, 0, c.s, tmp + n, v, c.perm, n, 1, 1);
+}
+
 // Right-preconditioned GMRES(restart) with MGS Arnoldi (oracle/h2.py: gmres); A = the H2
-// matvec, M^{-1} = the AIFMM solve (if precond).  b, x: device, user order, N x 1.
+// matvec, M^{-1} = the AIFMM solve (precond 1), the leaf block-diagonal inverse (precond 2) or
+// none (precond 0).  b, x: device, user order, N x 1.
 static void gmres_dev(Ctx& c, const double* b, double* x, int restart, double rtol, int maxit, int precond,
                       int* iters, double* relres) {
   const long long n = c.n;
@@ -1968,6 +2027,12 @@ static void gmres_dev(Ctx& c, const double* b, double* x, int restart, double rt
   double* y = P.d(restart);
   double* part = P.d(512);
   double* sc = P.d(8);   // 0: ||b||, 1: beta, 2: residual estimate
+  double* bdt = precond == 2 ? P.d((size_t)2 * n) : nullptr;
+  if (precond == 2) bd_prepare(c);
+  auto apply_precond = [&](double* v) {
+    if (precond == 1) solve_dev(c, v, 1);
+    else if (precond == 2) bd_apply(c, v, bdt);
+  };
   auto rd = [&](double* dp) {
     double h = 0;
     AIFMM_CUDA(cudaMemcpyAsync(&h, dp, sizeof(double), cudaMemcpyDeviceToHost, c.s));
@@ -1993,7 +2058,7 @@ static void gmres_dev(Ctx& c, const double* b, double* x, int restart, double rt
       const double* op = vj;
       if (precond) {
         vec_axpy(t, vj, n, nullptr, 1.0, 0.0, c.s);
-        solve_dev(c, t, 1);
+        apply_precond(t);
         op = t;
       }
       matvec_dev(c, op, w, 1);
@@ -2012,7 +2077,7 @@ static void gmres_dev(Ctx& c, const double* b, double* x, int restart, double rt
     }
     gm_backsub(H, ldh, g, y, j, c.s);
     gm_gemv(V, n, y, j, n, t, c.s);
-    if (precond) solve_dev(c, t, 1);
+    if (precond) apply_precond(t);
     vec_axpy(x, t, n, nullptr, 1.0, 1.0, c.s);
     matvec_dev(c, x, w, 1);                            // true residual at the restart
     vec_axpy(r, b, n, nullptr, 1.0, 0.0, c.s);
@@ -2120,6 +2185,8 @@ int aifmm_build(const double* points, int64_t n, int d, int kernel_id, const dou
   c.nn.clear();
   c.hnn.clear();
   c.h2_built = false;
+  c.bd_ready = false;
+  c.bdpool.reset();
   c.h2pool.reset();
   c.built = c.factored = false;
   c.n = n;
@@ -2148,6 +2215,13 @@ int aifmm_set_compression_tol(double tol_c) {
   CAPI_BEGIN
   AIFMM_REQUIRE(tol_c >= 0.0 && tol_c < 1.0, AIFMM_EINVALID_ARG, "tol_c must lie in [0,1)");
   ctx().tol_c_user = tol_c;
+  CAPI_END
+}
+
+int aifmm_set_algorithm(int alg) {
+  CAPI_BEGIN
+  AIFMM_REQUIRE(alg == 2 || alg == 3, AIFMM_EINVALID_ARG, "algorithm must be 2 or 3");
+  ctx().algorithm = alg;
   CAPI_END
 }
 
@@ -2248,6 +2322,8 @@ void aifmm_free(void) {
   c.nn.clear();
   c.hnn.clear();
   c.h2_built = false;
+  c.bd_ready = false;
+  c.bdpool.reset();
   c.h2pool.reset();
   c.h2work.reset();
   c.gmpool.reset();
@@ -2393,6 +2469,8 @@ int aifmm_matvec_build(double tol) {
   AIFMM_REQUIRE(c.built, AIFMM_ESTATE, "matvec_build before build");
   AIFMM_REQUIRE(tol > 0.0 && tol < 1.0, AIFMM_EINVALID_ARG, "tol must lie in (0,1)");
   c.h2_built = false;
+  c.bd_ready = false;
+  c.bdpool.reset();
   c.h2pool.reset();
   build_nnca(c, c.hnn, tol / 100.0, c.h2pool);   // reading R18: eps_ACA = tol / 100
   c.h2_tol = tol;
@@ -2414,7 +2492,8 @@ int aifmm_gmres(const double* b, double* x, int restart, double rtol, int maxit,
   CAPI_BEGIN
   Ctx& c = ctx();
   AIFMM_REQUIRE(c.h2_built, AIFMM_ESTATE, "gmres before matvec_build");
-  AIFMM_REQUIRE(!precond || c.factored, AIFMM_ESTATE, "preconditioned gmres before factor");
+  AIFMM_REQUIRE(precond >= 0 && precond <= 2, AIFMM_EINVALID_ARG, "precond must be 0, 1 or 2");
+  AIFMM_REQUIRE(precond != 1 || c.factored, AIFMM_ESTATE, "AIFMM-preconditioned gmres before factor");
   AIFMM_REQUIRE(b && x && iters && relres && restart >= 1 && maxit >= 1 && rtol > 0.0, AIFMM_EINVALID_ARG,
                 "bad gmres arguments");
   AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));

@@ -69,3 +69,30 @@ def test_gmres_preconditioned_parity_config5_style():
     # unpreconditioned GMRES needs more iterations on the same system
     _, it0, rr0 = G.gmres(torch.from_numpy(b).cuda(), restart=30, rtol=1e-10, maxit=it, precond=False)
     assert rr0 > 1e-10
+
+
+def test_gmres_three_preconditioners_parity():
+    """Row f3 (the paper's comparison I_G / I_BD / I_pA, table) on a
+    config-5-style 3D 1/r problem: GMRES with no preconditioner, the leaf block-diagonal inverse
+    and the AIFMM(1e-3) factor.  Each GPU iteration count is within one of the oracle's with the
+    same preconditioner, and the counts are ordered I_pA < I_BD <= I_G."""
+    n = 4000
+    pts = W.make_points("uniform_01", n, 3, 43)
+    b = W.make_rhs(n, 1, 43)[:, 0]
+    kp = (100.0, 0.0)
+    from oracle.h2 import block_diagonal_precond
+    h = H2(pts, 2, kp, 32, 1e-10)
+    P = Oracle(pts, 2, kp, 32, 1e-3).factor()
+    bd = block_diagonal_precond(P.tree, 2, kp)
+    G.free()
+    G.build(torch.from_numpy(pts).cuda(), 2, kp, 32, 1e-3)
+    G.factor()
+    G.matvec_build(1e-10)
+    its = {}
+    for name, pre_o, pre_g in (("G", None, 0), ("BD", bd, 2), ("pA", P.solve, 1)):
+        _, ito, rro = gmres(h.matvec, b, precond=pre_o, restart=30, rtol=1e-10, maxit=400)
+        _, it, rr = G.gmres(torch.from_numpy(b).cuda(), restart=30, rtol=1e-10, maxit=400, precond=pre_g)
+        assert rro <= 1e-10 and rr <= 1e-10, (name, rro, rr)
+        assert abs(it - ito) <= 1, (name, it, ito)
+        its[name] = it
+    assert its["pA"] < its["BD"] <= its["G"], its

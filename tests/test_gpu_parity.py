@@ -200,7 +200,77 @@ def test_gpu_residual_matches_oracle_direct_sum():
         for rr in (None, rows):
             ro = dense.residual(pts, kid, kp, x, b, rr)
             rg = G.residual(X, torch.from_numpy(b).cuda(), rr)
-            assert abs(rg - ro) <= 1e-9 * ro + 1e-15, (kid, rg, ro)
+            assert abs(rg - ro) <= 1e-9 * ro + 1e-13, (kid, rg, ro)   # 1e-13: rounding floor of A x - b
         # an exact solution of a perturbed system: residual of (X, A X) is ~0
         Y = torch.from_numpy(dense.dense_matrix(pts, kid, kp) @ x).cuda()
         assert G.residual(X, Y) <= 1e-13
+
+
+@pytest.mark.parametrize("case", CASES[:2] + CASES[4:5], ids=[c[0] for c in CASES[:2] + CASES[4:5]])
+def test_algorithm2_parity(case):
+    """Row f2: Algorithm 2 (compress on creation) on the GPU (aifmm_set_algorithm(2))
+    against the oracle's Algorithm 2: same number of compressions (integer), solution within
+    10*tol, residual within 2x."""
+    name, kind, n, d, kid, kp, leaf, tol, nrhs = case
+    pts = W.make_points(kind, n, d, 21)
+    b = W.make_rhs(n, nrhs, 21)
+    o = Oracle(pts, kid, kp, leaf, tol, algorithm=2).factor()
+    xo = o.solve(b)
+    G.set_algorithm(2)
+    try:
+        G.reset_counters()
+        x = _gpu_solve(pts, b, kid, kp, leaf, tol)
+        st = G.stats()
+    finally:
+        G.set_algorithm(3)
+    assert int(st["compressions"]) == o.stats["compressions"]
+    assert np.linalg.norm(x - xo) / np.linalg.norm(xo) <= 10 * tol
+    assert dense.residual(pts, kid, kp, x, b) <= 2 * dense.residual(pts, kid, kp, xo, b) + 1e-13
+
+
+def _golden(name):
+    p = os.path.join(os.path.dirname(__file__), "golden", f"{name}_oracle.npz")
+    if not os.path.exists(p):
+        pytest.skip(f"{p} not generated (tools/oracle_golden.py)")
+    g = np.load(p)
+    return g, json.loads(str(g["meta"]))
+
+
+def test_config3_full_size_parity():
+    """BASELINE config 3 at full size (N = 2^20 Matern, leaf 128, tol 1e-8, 1 RHS) in the
+    configuration bench.py times, against the serial C++ oracle's cached result
+    (tests/golden/cfg3_rand2d_matern_1M_oracle.npz, written by tools/oracle_golden.py on a GPU
+    box's host): integer outputs (tree, lists, colours, NNCA ranks) bit-exact with the C++
+    oracle's build (re-run here), solution within 10*tol of the oracle's, sampled direct-sum
+    residual within 2x the oracle's."""
+    from oracle.cpp import CppAIFMM
+    cfg = W.CONFIGS[2]
+    g, meta = _golden(cfg.name)
+    pts, b = W.make(cfg)
+    G.free()
+    G.build(torch.from_numpy(pts).cuda(), cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol)
+    c = CppAIFMM(pts, cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol, threads=os.cpu_count() or 1)
+    perm, L = G.get_tree(cfg.n)
+    assert L == c.L == meta["L"]
+    assert np.array_equal(perm, c.perm())
+    for l in range(2, L + 1):
+        assert np.array_equal(G.get_level_offsets(l, 2), c.offsets(l))
+        gn = G.get_lists(l, 2)
+        cn = c.lists(l)
+        for a, bb in zip(gn, cn):
+            assert np.array_equal(a, bb)
+        assert np.array_equal(G.get_colours(l, 2), c.colours(l))
+        assert np.array_equal(G.get_ranks(l, 2, 0), g[f"nnca_{l}"])
+    del c
+    G.factor()
+    X = G.solve(torch.from_numpy(np.ascontiguousarray(b)).cuda())
+    x = X.cpu().numpy()
+    xo = g["x"]
+    rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)
+    rows = W.residual_rows(cfg.n, cfg.seed)
+    rg = G.residual(X, torch.from_numpy(np.ascontiguousarray(b)).cuda(), rows)
+    ro = meta["residual_4096_rows"]
+    mism = {l: int(np.sum(G.get_ranks(l, 2, 1) != g[f"ranks_{l}"])) for l in range(2, L + 1)}
+    print(f"config 3: rel solution diff {rel:.3e}, residual {rg:.3e} (oracle {ro:.3e}), final-rank mismatches {mism}")
+    assert rg <= 2 * ro, (rg, ro)
+    assert rel <= 10 * cfg.tol, (rel, mism)

@@ -68,3 +68,22 @@ def test_aifmm_preconditioned_gmres_config5_style():
     assert rr0 > 1e-10
     A = dense.dense_matrix(pts, 2, kp)
     assert np.linalg.norm(A @ x - b) <= 1e-8 * np.linalg.norm(b)
+
+
+def test_block_diagonal_precond_inverts_leaf_blocks():
+    """oracle/h2.py: block_diagonal_precond applied to blockdiag(A) x gives x back (the dense
+    block-diagonal part written out from the exact matrix, same leaves), in user order."""
+    from oracle.h2 import block_diagonal_precond
+    from oracle.tree import Tree
+    pts, _ = W.small_problem(d=2, n=700, seed=3)
+    kp = (10.0, 0.0)
+    t = Tree(pts, 30)
+    leaf_of = np.empty(700, dtype=np.int64)
+    for b in t.nonempty(t.L):
+        a0, a1 = t.point_range(t.L, b)
+        leaf_of[t.perm[a0:a1]] = b
+    A = dense.dense_matrix(pts, 0, kp)
+    Abd = np.where(leaf_of[:, None] == leaf_of[None, :], A, 0.0)
+    x = np.random.default_rng(0).standard_normal(700)
+    M = block_diagonal_precond(t, 0, kp)
+    assert np.linalg.norm(M(Abd @ x) - x) <= 1e-10 * np.linalg.norm(x)
