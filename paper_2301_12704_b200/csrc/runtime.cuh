@@ -371,6 +371,7 @@ class GemmBatch {
     terms_.insert(terms_.end(), o.terms_.begin(), o.terms_.end());
   }
   GemmTerm& term_ref(size_t i) { return terms_[i]; }
+  GemmTask& task_ref(size_t i) { return tasks_[i]; }
   // Deterministic split-K: single-term tasks with a long K and few output tiles are split into
   // S partial GEMMs into workspace slices, then reduced in a fixed order by a second launch.
   void set_splitk_pool(DevPool* p) { splitk_ = p; }
@@ -615,13 +616,18 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   // off by default in the factorisation (measured: no gain on configs 2 and 3); the test hook
   // aifmm_debug_tri_root enables it for every m
   static const int tsqr_env = getenv("AIFMM_TSQR_MMAX") ? atoi(getenv("AIFMM_TSQR_MMAX")) : 0;
+  // chunk rows: HH_REG_ROWS (one-CTA register panels) by default; AIFMM_TSQR_ROWS (experiment)
+  static const int tsqr_rows = getenv("AIFMM_TSQR_ROWS") ? atoi(getenv("AIFMM_TSQR_ROWS")) : HH_REG_ROWS;
+  // only requests taller than this are split (experiment toggle; default: every n > chunk)
+  static const int tsqr_nmin = getenv("AIFMM_TSQR_NMIN") ? atoi(getenv("AIFMM_TSQR_NMIN")) : 0;
   const int tsqr_mmax = tsqr_m >= 0 ? tsqr_m : tsqr_env;
+  const int CHR = tsqr_m >= 0 ? HH_REG_ROWS : tsqr_rows;
   std::vector<TriRootReq> reqs, stacks;
   for (const TriRootReq& q : reqs_in) {
-    bool split = !no_tsqr && q.m >= 1 && q.m <= tsqr_mmax && q.n > HH_REG_ROWS;
+    bool split = !no_tsqr && q.m >= 1 && q.m <= tsqr_mmax && q.n > CHR && q.n > tsqr_nmin;
     int nch = 0, S = 0;
     if (split) {
-      nch = (q.n + HH_REG_ROWS - 1) / HH_REG_ROWS;
+      nch = (q.n + CHR - 1) / CHR;
       for (int c = 0; c < nch; ++c) S += std::min(q.n / nch + (c < q.n % nch ? 1 : 0), q.m);
       split = 5LL * S <= 4LL * q.n;
     }
