@@ -95,6 +95,24 @@ __global__ void permute_rows_kernel(const double* src, double* dst, const int* p
     else dst[c * n + j] = src[c * n + perm[j]];
   }
 }
+// deterministic pseudo-random fill (counter-based: splitmix64 of (seed, row, column)), uniform
+// in [-1, 1): the test matrix Omega of the null-space pivot formation (R31)
+struct HashFillTask { double* dst; int ld, rows, cols; unsigned long long seed; };
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void hash_fill_kernel(const HashFillTask* __restrict__ t) {
+  const HashFillTask k = t[blockIdx.x];
+  const long long tot = (long long)k.rows * k.cols;
+  for (long long e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int i = (int)(e % k.rows), j = (int)(e / k.rows);
+    const unsigned long long h = splitmix64(k.seed ^ splitmix64(((unsigned long long)i << 32) | (unsigned)j));
+    k.dst[(size_t)j * k.ld + i] = (double)(h >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+  }
+}
 __global__ void finite_kernel(const double* a, long long n, int* flag) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     if (!isfinite(a[i])) *flag = 1;
@@ -643,8 +661,8 @@ static void setup_level(Ctx& c, int l) {
     // compression grows ranks by ~1-1.5x the NNCA rank (measured); regrow() handles the rest
     f.kcap[b] = std::min(f.m[b], 2 * f.k[b] + 16);
   }
-  f.dinfo = c.persist.i(nb);   // checked once at the end of the factorisation (no level-end sync)
-  AIFMM_CUDA(cudaMemsetAsync(f.dinfo, 0, sizeof(int) * nb, c.s));
+  f.dinfo = c.persist.i(2 * nb);   // checked once at the end of the factorisation (no level-end sync)
+  AIFMM_CUDA(cudaMemsetAsync(f.dinfo, 0, sizeof(int) * 2 * nb, c.s));   // [nb, 2nb): R31 CholeskyQR
   // zero-initialised capacity storage: U, V, Ud, Vd, far A, far F
   // zero-initialised blocks are carved from the level pool; consecutive carvings are
   // contiguous within a chunk, so the memset runs over few ranges
@@ -1324,6 +1342,122 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
   g_prof.hlap("tg.tasks");
 }
 
+// Reading R31 (null-space formation of the pivot inverse).  For P = [[K, U], [U^T, 0]] with
+// orthonormal U (m x k, R13; V = U, R27) and N any well-conditioned basis of the orthogonal
+// complement of range(U) (m x (m-k)), block elimination in the basis [U, N] gives, with
+// D = N^T K N:
+//   G11 = N D^{-1} N^T,   G12 = U - G11 K U,   G21 = U^T - U^T K G11,
+//   G22 = -U^T K U + U^T K G11 K U
+// (exact; independent of the choice of N).  The only inverse is D, of size m - k instead of
+// m + k; everything else is a DMMA GEMM.  N = Y R^{-1} with Y = (I - U U^T) Omega (Omega a fixed
+// counter-based pseudo-random m x (m-k) matrix) and Y^T Y = R^T R (one CholeskyQR pass: cond(N)
+// = 1 + O(eps cond(Y)^2)), re-projected against U once.  G is written into the record r.G exactly
+// where the explicit inverse went, so the multipliers, new blocks and the solve are unchanged.
+static void nullspace_pivots(Ctx& c, FLevel& f, const std::vector<int>& cs, const std::vector<int>& ns, FlopCounter& fp) {
+  const size_t nb = ns.size();
+  struct NS { double *Y, *t1, *Gm, *R1, *R1i, *N, *t4, *KN, *KU, *D, *Y1, *t, *t3; int m, k, p, n; const double* U; Blk K; double* G; };
+  std::vector<NS> v(nb);
+  std::vector<HashFillTask> hf;
+  int pmax = 1;
+  for (size_t x = 0; x < nb; ++x) {
+    const int i = cs[ns[x]];
+    NS& e = v[x];
+    e.m = f.m[i];
+    e.k = f.k[i];
+    e.p = e.m - e.k;
+    e.n = e.m + e.k;
+    e.U = f.U[i];
+    e.K = f.nearb.at(f.key(i, i));
+    e.G = f.rec[i].G;
+    const size_t mp = (size_t)e.m * e.p, pp = (size_t)e.p * e.p;
+    e.Y = c.work.d(mp);
+    e.t1 = c.work.d((size_t)e.k * e.p);
+    e.Gm = c.work.d(pp);
+    e.R1 = c.work.d(pp);
+    e.R1i = c.work.d(pp);
+    e.N = c.work.d(mp);
+    e.t4 = c.work.d((size_t)e.k * e.p);
+    e.KN = c.work.d(mp);
+    e.KU = c.work.d((size_t)e.m * e.k);
+    e.D = c.work.d(pp);
+    e.Y1 = c.work.d(mp);
+    e.t = c.work.d((size_t)e.p * e.k);
+    e.t3 = c.work.d((size_t)e.k * e.p);
+    pmax = std::max(pmax, e.p);
+    hf.push_back(HashFillTask{e.Y, e.m, e.m, e.p, 0x5EEDull * 0x100000001ull + (unsigned long long)e.m * 7919ull + e.p});
+  }
+  {
+    const HashFillTask* dh = c.up.put(hf);
+    LAUNCH(hash_fill_kernel, (int)nb, 256, 0, c.s, dh);
+  }
+  GemmBatch g;
+  // Y = Omega - U (U^T Omega)
+  for (auto& e : v) { g.task(e.t1, e.k, e.k, e.p, 0.0); g.term(1.0, e.U, e.m, 1, e.Y, e.m, 0, e.m); }
+  g.run(c.up, c.s, &fp);
+  for (auto& e : v) { g.task(e.Y, e.m, e.m, e.p, 1.0); g.term(-1.0, e.U, e.m, 0, e.t1, e.k, 0, e.k); }
+  g.run(c.up, c.s, &fp);
+  // CholeskyQR: Y^T Y = R^T R, N = Y R^{-1}, N -= U (U^T N)
+  for (auto& e : v) { g.task(e.Gm, e.p, e.p, e.p, 0.0); g.term(1.0, e.Y, e.m, 1, e.Y, e.m, 0, e.m); }
+  g.run(c.up, c.s, &fp);
+  {
+    std::vector<CholTask> ct;
+    for (size_t x = 0; x < nb; ++x) ct.push_back(CholTask{v[x].Gm, v[x].R1, v[x].R1i, v[x].p, 0, f.dinfo + f.nb + cs[ns[x]]});
+    launch_chol_inv(c.up.put(ct), (int)ct.size(), pmax, c.s);
+  }
+  for (auto& e : v) { g.task(e.N, e.m, e.m, e.p, 0.0); g.term(1.0, e.Y, e.m, 0, e.R1i, e.p, 0, e.p); }
+  g.run(c.up, c.s, &fp);
+  for (auto& e : v) { g.task(e.t4, e.k, e.k, e.p, 0.0); g.term(1.0, e.U, e.m, 1, e.N, e.m, 0, e.m); }
+  g.run(c.up, c.s, &fp);
+  for (auto& e : v) { g.task(e.N, e.m, e.m, e.p, 1.0); g.term(-1.0, e.U, e.m, 0, e.t4, e.k, 0, e.k); }
+  g.run(c.up, c.s, &fp);
+  // K N, K U
+  for (auto& e : v) {
+    g.task(e.KN, e.m, e.m, e.p, 0.0);
+    g.term(1.0, e.K.p, e.K.ld, 0, e.N, e.m, 0, e.m);
+    g.task(e.KU, e.m, e.m, e.k, 0.0);
+    g.term(1.0, e.K.p, e.K.ld, 0, e.U, e.m, 0, e.m);
+  }
+  g.run(c.up, c.s, &fp);
+  // D = N^T K N; t3 = U^T K N; G22 <- -U^T K U (completed below)
+  for (auto& e : v) {
+    g.task(e.D, e.p, e.p, e.p, 0.0);
+    g.term(1.0, e.N, e.m, 1, e.KN, e.m, 0, e.m);
+    g.task(e.t3, e.k, e.k, e.p, 0.0);
+    g.term(1.0, e.U, e.m, 1, e.KN, e.m, 0, e.m);
+  }
+  g.run(c.up, c.s, &fp);
+  {
+    std::vector<InvReq> inv;
+    for (size_t x = 0; x < nb; ++x) inv.push_back(InvReq{v[x].D, v[x].p, v[x].p, f.dinfo + cs[ns[x]]});
+    batched_inverse(inv, c.work, c.up, c.s, &fp);
+  }
+  // Y1 = D^{-1} N^T
+  for (auto& e : v) { g.task(e.Y1, e.p, e.p, e.m, 0.0); g.term(1.0, e.D, e.p, 0, e.N, e.m, 1, e.p); }
+  g.run(c.up, c.s, &fp);
+  // G11 = N Y1 (into G[0:m, 0:m]); t = Y1 K U
+  for (auto& e : v) {
+    g.task(e.G, e.n, e.m, e.m, 0.0);
+    g.term(1.0, e.N, e.m, 0, e.Y1, e.p, 0, e.p);
+    g.task(e.t, e.p, e.p, e.k, 0.0);
+    g.term(1.0, e.Y1, e.p, 0, e.KU, e.m, 0, e.m);
+  }
+  g.run(c.up, c.s, &fp);
+  // G12 = U - N t;  G21 = U^T - t3 Y1;  G22 = -U^T K U + t3 t
+  for (auto& e : v) {
+    g.task(e.G + (size_t)e.m * e.n, e.n, e.m, e.k, 0.0);
+    g.add(1.0, e.U, e.m, 0);
+    g.term(-1.0, e.N, e.m, 0, e.t, e.p, 0, e.p);
+    g.task(e.G + e.m, e.n, e.k, e.m, 0.0);
+    g.add(1.0, e.U, e.m, 1);
+    g.term(-1.0, e.t3, e.k, 0, e.Y1, e.p, 0, e.p);
+    g.task(e.G + (size_t)e.m * e.n + e.m, e.n, e.k, e.k, 0.0);
+    g.term(-1.0, e.U, e.m, 1, e.KU, e.m, 0, e.m);
+    g.term(1.0, e.t3, e.k, 0, e.t, e.p, 0, e.p);
+  }
+  g.run(c.up, c.s, &fp);
+  for (auto& e : v) c.fcp[PH_PIVOT].bytes += 8.0 * ((double)e.m * e.m + (double)e.m * e.k + (double)e.n * e.n);
+}
+
 // Steps 1-2 of a colour's elimination: pivot inverses and W_i = G[:, 0:m] R_i.  They need only
 // the colour's final bases and near blocks (no far M2L block), so they are launched before the
 // redirection of the colour's compression is planned.
@@ -1332,9 +1466,12 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   const int l = f.l;
   (void)l;
   if (g_prof.on) g_prof.begin(c.s);
-  // 1. assemble P_i = [[K_ii, U_i],[V_i^T, 0]] into G_i and invert in place (R16)
+  // 1. G_i = P_i^{-1}, P_i = [[K_ii, U_i],[V_i^T, 0]] (R16).  Boxes with 0 < k < m: null-space
+  //    formation (R31, below); the others (k = 0: P = K; k = m, R28): assembled and inverted.
   CopyBatch cb;
   std::vector<InvReq> inv;
+  std::vector<int> ns;   // colour positions a of the null-space boxes
+  static const bool no_ns = getenv("AIFMM_NO_NULLSPACE") != nullptr;   // debug toggle (R31 off)
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];
     const int m = f.m[i], k = f.k[i], n = m + k;
@@ -1343,6 +1480,7 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     r.k = k;
     r.G = c.persist.d(std::max<size_t>((size_t)n * n, 1));
     if (!n) continue;
+    if (k > 0 && k < m && !no_ns) { ns.push_back((int)a); continue; }
     const Blk& K = f.nearb.at(f.key(i, i));
     cb.copy(K.p, K.ld, r.G, n, m, m);
     cb.copy(f.U[i], m, r.G + (size_t)m * n, n, m, k);
@@ -1355,9 +1493,10 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     PhaseTimer pt(c, PH_PIVOT);
     FlopCounter fp;
     batched_inverse(inv, c.work, c.up, c.s, &fp);
+    for (const InvReq& r : inv) c.fcp[PH_PIVOT].bytes += 16.0 * r.n * r.n;   // read + write each pivot once
+    if (!ns.empty()) nullspace_pivots(c, f, cs, ns, fp);
     c.fc_all.flops += fp.flops;
     c.fcp[PH_PIVOT].flops += fp.flops;
-    for (const InvReq& r : inv) c.fcp[PH_PIVOT].bytes += 16.0 * r.n * r.n;   // read + write each pivot once
   }
   static const bool dbg_g11 = getenv("AIFMM_DEBUG_G11") != nullptr;   // debug: |G11| of full boxes (R28)
   if (dbg_g11) {
@@ -1410,6 +1549,44 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   if (g_prof.on) g_prof.end("elim.W");
 }
 
+// debug (AIFMM_DEBUG_SYM=1): largest |B_pq - B_qp^T| / max|B_pq| over the near, M2L and pending
+// fill-in blocks of the level (the symmetric system keeps every pair transposed, R27 / R30)
+static void dbg_symmetry(Ctx& c, FLevel& f, const char* where) {
+  double worst[3] = {0, 0, 0};
+  int wp[3] = {-1, -1, -1}, wq[3] = {-1, -1, -1};
+  for (int p : f.boxes)
+    for (int kind = 0; kind < 3; ++kind) {
+      int ni;
+      const int* li = kind == 0 ? c.nlist(f.l, p, &ni) : c.ilist(f.l, p, &ni);
+      for (int t = 0; t < ni; ++t) {
+        const int q = li[t];
+        if (q <= p) continue;
+        BlkTable& T = kind == 0 ? f.nearb : (kind == 1 ? f.A : f.F);
+        const Blk* a = T.get(f.key(p, q));
+        const Blk* b = T.get(f.key(q, p));
+        if (!a || !b) continue;
+        if (kind == 2 && !f.pending.count({p, q})) continue;
+        const int M = kind == 1 ? f.k[p] : live(f, p), N = kind == 1 ? f.k[q] : live(f, q);
+        if (!M || !N) continue;
+        std::vector<double> ha((size_t)a->ld * N), hb((size_t)b->ld * M);
+        AIFMM_CUDA(cudaMemcpyAsync(ha.data(), a->p, sizeof(double) * ha.size(), cudaMemcpyDeviceToHost, c.s));
+        AIFMM_CUDA(cudaMemcpyAsync(hb.data(), b->p, sizeof(double) * hb.size(), cudaMemcpyDeviceToHost, c.s));
+        c.up.sync();
+        double mx = 0, df = 0;
+        for (int j = 0; j < N; ++j)
+          for (int i = 0; i < M; ++i) {
+            const double x = ha[(size_t)j * a->ld + i], y = hb[(size_t)i * b->ld + j];
+            mx = std::max(mx, std::fabs(x));
+            df = std::max(df, std::fabs(x - y));
+          }
+        const double r = mx > 0 ? df / mx : df;
+        if (r > worst[kind]) { worst[kind] = r; wp[kind] = p; wq[kind] = q; }
+      }
+    }
+  fprintf(stderr, "[aifmm sym] level %d %s: near %.2e (%d,%d)  M2L %.2e (%d,%d)  fill %.2e (%d,%d)\n", f.l, where, worst[0], wp[0],
+          wq[0], worst[1], wp[1], wq[1], worst[2], wp[2], wq[2]);
+}
+
 static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
   g_expose.set("elim.upd");
   const int l = f.l;
@@ -1437,10 +1614,11 @@ static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     GemmTask& tk = P.g.task_ref(mr.task);
     tk.C = mtmp[t];
     tk.ldc = mr.M;
+    // the temporary already holds -T_pq (the planned terms carry alpha = -1)
     gm.task(mr.pq.p, mr.pq.ld, mr.M, mr.N, 1.0);
-    gm.add(-1.0, mtmp[t], mr.M, 0);
+    gm.add(1.0, mtmp[t], mr.M, 0);
     gm.task(mr.qp.p, mr.qp.ld, mr.N, mr.M, 1.0);
-    gm.add(-1.0, mtmp[t], mr.M, 1);
+    gm.add(1.0, mtmp[t], mr.M, 1);
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c.timing) {
@@ -1521,10 +1699,11 @@ static void deferred_checks(Ctx& c) {
   for (int l = c.L; l >= 2 && l < (int)c.fl.size(); --l) {
     const FLevel& fl = c.fl[l];
     if (!fl.dinfo) continue;
-    std::vector<int> info = d2h(c, fl.dinfo, fl.nb);
+    std::vector<int> info = d2h(c, fl.dinfo, 2 * (size_t)fl.nb);
     for (int b : fl.boxes)
-      if (info[b])
-        throw Error(AIFMM_ESINGULAR_PIVOT, "singular pivot at level " + std::to_string(l) + " box " + std::to_string(b));
+      if (info[b] || info[fl.nb + b])
+        throw Error(AIFMM_ESINGULAR_PIVOT, std::string(info[b] ? "singular pivot" : "null-space basis (R31) not of full rank") +
+                                               " at level " + std::to_string(l) + " box " + std::to_string(b));
   }
 }
 
@@ -1554,6 +1733,7 @@ static void factor_levels(Ctx& c) {
     g_prof.begin(c.s);
     orthonormalise(c, f);
     g_prof.end("orth");
+    if (getenv("AIFMM_DEBUG_SYM")) dbg_symmetry(c, f, "after setup");
     int ncol = 0;
     for (int b : f.boxes) ncol = std::max(ncol, c.col[l][b] + 1);
     for (int col = 0; col < ncol; ++col) {
@@ -1572,6 +1752,8 @@ static void factor_levels(Ctx& c) {
       g_prof.begin(c.s);
       eliminate_update(c, f, cs, plan);
       g_prof.end(("eliminate.L" + std::to_string(l)).c_str());
+      static const bool dbg_sym = getenv("AIFMM_DEBUG_SYM") != nullptr;
+      if (dbg_sym) dbg_symmetry(c, f, ("after colour " + std::to_string(col)).c_str());
       if (c.algorithm == 2 && !f.pending.empty()) {   // Alg. 2: compress on creation (R29)
         std::vector<std::pair<int, int>> all(f.pending.begin(), f.pending.end());
         compress(c, f, all, [] {});
