@@ -1238,7 +1238,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
 // offset and patched once n_i = m_i + k_i is known.
 struct SchurPlan {
   GemmBatch g;
-  struct Fix { size_t term; int a, off; };
+  struct Fix { size_t term; int a, off, pidx; };
   std::vector<Fix> fix;
   std::vector<std::vector<int>> nbs;
   std::vector<std::vector<std::pair<int, int>>> wcol;   // (q, column offset in W_i)
@@ -1250,6 +1250,11 @@ struct SchurPlan {
   // eliminate_update) and applied as (p,q) -= T_pq and (q,p) -= T_pq^T
   struct Mirror { size_t task; Blk pq, qp; int M, N; };
   std::vector<Mirror> mir;
+  // R31 low-rank Schur terms of the null-space boxes: G11 = N Y1 (Y1 = D^{-1} N^T), so
+  // C_p G11 R_q = (C_p N)(Y1 R_q) with inner dimension m - k instead of m
+  std::vector<int> pdim;                    // m - k of a null-space box, 0 otherwise
+  std::vector<double*> Nb, Y1b, Rh;         // N (m x p), Y1 (p x m), Rh = Y1 [R_q ...] (p x tot)
+  std::vector<std::vector<double*>> Ch;     // C_p N (live_p x p) per neighbour p (order of nbs[a])
 };
 static int wcol_of(const std::vector<std::pair<int, int>>& w, int q) {
   for (auto& e : w)
@@ -1309,6 +1314,10 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
       t0 = t1;
       if (grp_a.empty()) continue;
       const int M = live(f, p), N = live(f, q);
+      // a far pair touched by the colour becomes pending even when one of its live sizes is 0
+      // (as in the oracle: its compression then adds nothing, but it is counted)
+      if (!f.nearb.get(f.key(p, q)) && !(f.E[p] && f.E[q]) && p < q)
+        P.new_pending.push_back({p, q});
       if (!M || !N) continue;
       // R30: the (p, q) and (q, p) updates are transposes (symmetric kernel, V = U, R27); the
       // pair is planned once, at p < q (the contributing boxes are the same for both)
@@ -1324,7 +1333,6 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
         return T;
       };
       Blk T = target(p, q);
-      if (!f.nearb.get(f.key(p, q)) && !(f.E[p] && f.E[q])) P.new_pending.push_back({std::min(p, q), std::max(p, q)});
       if (p < q && !no_sym) {
         P.mir.push_back({P.g.size(), T, target(q, p), M, N});
         P.g.task(nullptr, M, M, N, 0.0);   // temporary T_pq, allocated in eliminate_update
@@ -1334,7 +1342,9 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
       for (int a : grp_a) {
         const int i = cs[a];
         const Blk& C = f.nearb.at(f.key(p, i));
-        P.fix.push_back({P.g.nterms(), a, wcol_of(P.wcol[a], q)});
+        int pidx = 0;
+        while (P.nbs[a][pidx] != p) ++pidx;
+        P.fix.push_back({P.g.nterms(), a, wcol_of(P.wcol[a], q), pidx});
         P.g.term(-1.0, C.p, C.ld, 0, nullptr, 0, 0, f.m[i]);   // B patched in eliminate_colour
       }
     }
@@ -1353,7 +1363,8 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
 // counter-based pseudo-random m x (m-k) matrix) and Y^T Y = R^T R (one CholeskyQR pass: cond(N)
 // = 1 + O(eps cond(Y)^2)), re-projected against U once.  G is written into the record r.G exactly
 // where the explicit inverse went, so the multipliers, new blocks and the solve are unchanged.
-static void nullspace_pivots(Ctx& c, FLevel& f, const std::vector<int>& cs, const std::vector<int>& ns, FlopCounter& fp) {
+static void nullspace_pivots(Ctx& c, FLevel& f, const std::vector<int>& cs, const std::vector<int>& ns, FlopCounter& fp,
+                             SchurPlan& P) {
   const size_t nb = ns.size();
   struct NS { double *Y, *t1, *Gm, *R1, *R1i, *N, *t4, *KN, *KU, *D, *Y1, *t, *t3; int m, k, p, n; const double* U; Blk K; double* G; };
   std::vector<NS> v(nb);
@@ -1456,6 +1467,11 @@ static void nullspace_pivots(Ctx& c, FLevel& f, const std::vector<int>& cs, cons
   }
   g.run(c.up, c.s, &fp);
   for (auto& e : v) c.fcp[PH_PIVOT].bytes += 8.0 * ((double)e.m * e.m + (double)e.m * e.k + (double)e.n * e.n);
+  for (size_t x = 0; x < nb; ++x) {
+    P.pdim[ns[x]] = v[x].p;
+    P.Nb[ns[x]] = v[x].N;
+    P.Y1b[ns[x]] = v[x].Y1;
+  }
 }
 
 // Steps 1-2 of a colour's elimination: pivot inverses and W_i = G[:, 0:m] R_i.  They need only
@@ -1471,7 +1487,9 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   CopyBatch cb;
   std::vector<InvReq> inv;
   std::vector<int> ns;   // colour positions a of the null-space boxes
-  static const bool no_ns = getenv("AIFMM_NO_NULLSPACE") != nullptr;   // debug toggle (R31 off)
+  // R31 is opt-in (AIFMM_NULLSPACE=1): measured slower on configs 2 and 3 (its one-CTA Cholesky
+  // of the (m-k) x (m-k) Gram matrix is latency-bound), see DESIGN.md
+  static const bool no_ns = getenv("AIFMM_NULLSPACE") == nullptr;
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];
     const int m = f.m[i], k = f.k[i], n = m + k;
@@ -1494,7 +1512,10 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     FlopCounter fp;
     batched_inverse(inv, c.work, c.up, c.s, &fp);
     for (const InvReq& r : inv) c.fcp[PH_PIVOT].bytes += 16.0 * r.n * r.n;   // read + write each pivot once
-    if (!ns.empty()) nullspace_pivots(c, f, cs, ns, fp);
+    P.pdim.assign(cs.size(), 0);
+    P.Nb.assign(cs.size(), nullptr);
+    P.Y1b.assign(cs.size(), nullptr);
+    if (!ns.empty()) nullspace_pivots(c, f, cs, ns, fp, P);
     c.fc_all.flops += fp.flops;
     c.fcp[PH_PIVOT].flops += fp.flops;
   }
@@ -1528,20 +1549,42 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
               f.m[mx[t].second], f.k[mx[t].second], mx[t].first);
   }
   if (g_prof.on) { g_prof.end("elim.inverse"); g_prof.begin(c.s); }
-  // 2. W_i = G[:, 0:m] * R_i (row X_i blocks), columns ordered as N(i) \ i
+  // 2. W_i = G[:, 0:m] * R_i (row X_i blocks), columns ordered as N(i) \ i.  Null-space boxes
+  //    (R31): only W_z = G[m:, 0:m] R_i (the new (Z_i, x_q) blocks); their Schur terms use
+  //    Rh = Y1 R_i and Ch_p = C_p N instead of W[0:m]
   std::vector<double*> W(cs.size());
+  P.Rh.assign(cs.size(), nullptr);
+  P.Ch.assign(cs.size(), {});
   GemmBatch g;
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];
-    const int m = f.m[i], n = m + f.k[i];
+    const int m = f.m[i], k = f.k[i], n = m + k, pd = P.pdim[a];
     W[a] = c.work.d(std::max<size_t>((size_t)n * P.tot[a], 1));
     if (!n) continue;
+    if (pd) P.Rh[a] = c.work.d(std::max<size_t>((size_t)pd * P.tot[a], 1));
     for (auto& wq : P.wcol[a]) {
       const int q = wq.first;
       const Blk& R = f.nearb.at(f.key(i, q));
       if (!live(f, q)) continue;
-      g.task(W[a] + (size_t)wq.second * n, n, n, live(f, q), 0.0);
-      g.term(1.0, f.rec[i].G, n, 0, R.p, R.ld, 0, m);
+      if (!pd) {
+        g.task(W[a] + (size_t)wq.second * n, n, n, live(f, q), 0.0);
+        g.term(1.0, f.rec[i].G, n, 0, R.p, R.ld, 0, m);
+      } else {
+        g.task(W[a] + (size_t)wq.second * n + m, n, k, live(f, q), 0.0);
+        g.term(1.0, f.rec[i].G + m, n, 0, R.p, R.ld, 0, m);
+        g.task(P.Rh[a] + (size_t)wq.second * pd, pd, pd, live(f, q), 0.0);
+        g.term(1.0, P.Y1b[a], pd, 0, R.p, R.ld, 0, m);
+      }
+    }
+    if (pd) {
+      for (int p : P.nbs[a]) {
+        const Blk& C = f.nearb.at(f.key(p, i));
+        double* ch = c.work.d(std::max<size_t>((size_t)live(f, p) * pd, 1));
+        P.Ch[a].push_back(ch);
+        if (!live(f, p)) continue;
+        g.task(ch, live(f, p), live(f, p), pd, 0.0);
+        g.term(1.0, C.p, C.ld, 0, P.Nb[a], m, 0, m);
+      }
     }
   }
   g.run(c.up, c.s, &c.fc_all);
@@ -1601,8 +1644,18 @@ static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     const int i = cs[fx.a];
     const int n = f.m[i] + f.k[i];
     GemmTerm& t = P.g.term_ref(fx.term);
-    t.B = W[fx.a] + (size_t)fx.off * n;
-    t.ldb = n;
+    const int pd = P.pdim.empty() ? 0 : P.pdim[fx.a];
+    if (pd) {   // R31: (C_p N)(Y1 R_q)
+      const int p = P.nbs[fx.a][fx.pidx];
+      t.A = P.Ch[fx.a][fx.pidx];
+      t.lda = std::max(live(f, p), 1);
+      t.B = P.Rh[fx.a] + (size_t)fx.off * pd;
+      t.ldb = pd;
+      t.K = pd;
+    } else {
+      t.B = W[fx.a] + (size_t)fx.off * n;
+      t.ldb = n;
+    }
   }
   for (auto& pr : P.new_pending) f.pending.insert(pr);
   // R30 temporaries (the work pool is not reset between here and the end of the colour)
