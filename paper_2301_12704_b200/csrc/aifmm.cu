@@ -1288,7 +1288,9 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
   g_prof.hlap("tg.sort");
   std::vector<std::pair<int, int>> qa;   // (q, a) of one target row p
   std::vector<int> grp_a;
-  static const bool no_sym = getenv("AIFMM_NO_SYM_SCHUR") != nullptr;   // debug toggle (R30 off)
+  // R30 is opt-in (AIFMM_SYM_SCHUR=1): half the Schur flops, but measured slower end to end on
+  // configs 2 and 3 (the factorisation then takes larger ranks)
+  static const bool no_sym = getenv("AIFMM_SYM_SCHUR") == nullptr;
   for (int p = 0; p < f.nb; ++p) {
     if (!isp[p]) continue;
     qa.clear();
@@ -1308,7 +1310,9 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
         // R28: a box whose basis spans R^m (k = m) when its colour begins (this plan precedes
         // the colour's compression) has G11 = 0 -- no Schur term, no fill-in
         static const bool no_r28 = getenv("AIFMM_NO_R28") != nullptr;   // debug toggle
-        if (f.m[cs[a]] && (no_r28 || f.k[cs[a]] < f.m[cs[a]])) grp_a.push_back(a);
+        // (a box with m = 0 contributes nothing but, as in the oracle, still makes its far
+        // neighbour pairs pending; its zero-size terms are dropped below)
+        if (!f.m[cs[a]] || no_r28 || f.k[cs[a]] < f.m[cs[a]]) grp_a.push_back(a);
       }
       const int q = qa[t0].first;
       t0 = t1;
@@ -1341,6 +1345,7 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
       }
       for (int a : grp_a) {
         const int i = cs[a];
+        if (!f.m[i]) continue;
         const Blk& C = f.nearb.at(f.key(p, i));
         int pidx = 0;
         while (P.nbs[a][pidx] != p) ++pidx;

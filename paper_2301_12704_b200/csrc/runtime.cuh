@@ -613,18 +613,20 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   // signs of its rows, which the pivoted QR of the second stage (on R^T's columns) does not see.
   // Every chunk panel then lives in registers (hh_panel_reg_kernel).
   static const bool no_tsqr = getenv("AIFMM_NO_TSQR") != nullptr;   // debug toggle
-  // off by default in the factorisation (measured: no gain on configs 2 and 3); the test hook
-  // aifmm_debug_tri_root enables it for every m
-  static const int tsqr_env = getenv("AIFMM_TSQR_MMAX") ? atoi(getenv("AIFMM_TSQR_MMAX")) : 0;
-  // chunk rows: HH_REG_ROWS (one-CTA register panels) by default; AIFMM_TSQR_ROWS (experiment)
-  static const int tsqr_rows = getenv("AIFMM_TSQR_ROWS") ? atoi(getenv("AIFMM_TSQR_ROWS")) : HH_REG_ROWS;
-  // only requests taller than this are split (experiment toggle; default: every n > chunk)
-  static const int tsqr_nmin = getenv("AIFMM_TSQR_NMIN") ? atoi(getenv("AIFMM_TSQR_NMIN")) : 0;
+  // the test hook aifmm_debug_tri_root forces chunks of HH_REG_ROWS rows for every request
+  // Default (measured on config 3: factor -11%, config 2 neutral; chunks of 1024 / 2048 rows
+  // were slower): requests taller than HH_REGCL_ROWS are split into balanced chunks of at most
+  // HH_REGCL_ROWS rows, so every chunk panel lives in registers of an 8-CTA cluster instead of
+  // running the global-memory cluster panel.  AIFMM_TSQR_{MMAX,ROWS,NMIN} override (experiments).
+  static const int tsqr_env = getenv("AIFMM_TSQR_MMAX") ? atoi(getenv("AIFMM_TSQR_MMAX")) : (1 << 30);
+  static const int tsqr_rows = getenv("AIFMM_TSQR_ROWS") ? atoi(getenv("AIFMM_TSQR_ROWS")) : HH_REGCL_ROWS;
+  static const int tsqr_nmin = getenv("AIFMM_TSQR_NMIN") ? atoi(getenv("AIFMM_TSQR_NMIN")) : HH_REGCL_ROWS;
   const int tsqr_mmax = tsqr_m >= 0 ? tsqr_m : tsqr_env;
   const int CHR = tsqr_m >= 0 ? HH_REG_ROWS : tsqr_rows;
+  const int NMIN = tsqr_m >= 0 ? 0 : tsqr_nmin;
   std::vector<TriRootReq> reqs, stacks;
   for (const TriRootReq& q : reqs_in) {
-    bool split = !no_tsqr && q.m >= 1 && q.m <= tsqr_mmax && q.n > CHR && q.n > tsqr_nmin;
+    bool split = !no_tsqr && q.m >= 1 && q.m <= tsqr_mmax && q.n > CHR && q.n > NMIN;
     int nch = 0, S = 0;
     if (split) {
       nch = (q.n + CHR - 1) / CHR;
