@@ -722,55 +722,51 @@ __global__ void gj_unscramble_kernel(const GJBTask* __restrict__ tasks) {
 // gives the same exact change of variables).  One CTA per matrix, in shared memory up to
 // CHOL_SMEM_MAX, else in global memory (in place).  info = 1 + step of a non-positive pivot.
 constexpr int CHOL_NT = 256;
-__device__ int chol_inv_device(double* S, int ld, int k, double* tmp) {
+// Lower Cholesky G = L L^T in place (column-major, ld), column oriented: column j is scaled,
+// then every trailing column c > j is updated along its contiguous rows i >= c (one warp per
+// column, lanes over rows: coalesced).  Returns 0 or 1 + the step of a non-positive pivot.
+__device__ int chol_lower_device(double* S, int ld, int k) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ int bad;
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  // right-looking upper Cholesky: row j of R = (row j of the trailing G) / sqrt(pivot)
   for (int j = 0; j < k; ++j) {
     const double piv = S[(size_t)j * ld + j];
-    if (!(piv > 0.0)) {
-      if (tid == 0) bad = j + 1;
-      __syncthreads();
-      return bad;
-    }
+    if (!(piv > 0.0)) return j + 1;                 // uniform: every thread read the same value
     const double d = sqrt(piv);
+    double* cj = S + (size_t)j * ld;
     __syncthreads();
-    for (int c = j + 1 + tid; c < k; c += CHOL_NT) S[(size_t)c * ld + j] /= d;
+    for (int i = j + 1 + tid; i < k; i += CHOL_NT) cj[i] /= d;
+    if (tid == 0) cj[j] = d;
     __syncthreads();
-    if (tid == 0) S[(size_t)j * ld + j] = d;
-    // trailing update of the upper triangle: G[r, c] -= R[j, r] R[j, c], r <= c
     for (int c = j + 1 + warp; c < k; c += CHOL_NT / 32) {
-      const double rc = S[(size_t)c * ld + j];
-      for (int r = j + 1 + lane; r <= c; r += 32) S[(size_t)c * ld + r] -= S[(size_t)r * ld + j] * rc;
+      const double lc = cj[c];
+      double* cc = S + (size_t)c * ld;
+      for (int i = c + lane; i < k; i += 32) cc[i] -= cj[i] * lc;
     }
     __syncthreads();
   }
-  // zero the strict lower triangle (R is upper)
-  for (int c = warp; c < k; c += CHOL_NT / 32)
-    for (int r = c + 1 + lane; r < k; r += 32) S[(size_t)c * ld + r] = 0.0;
-  __syncthreads();
   return 0;
 }
-// in-place inverse of an upper-triangular matrix (column by column, dtrti2 order)
-__device__ void trtri_upper_device(double* S, int ld, int k, double* tmp) {
+// In-place inverse X = L^{-1} of a lower-triangular L (column-major), dtrti2 order: for
+// j = k-1 .. 0, X(j+1:, j) = -X(j,j) X(j+1:, j+1:) L(j+1:, j); threads over the rows i read
+// X(i, l) for consecutive i at fixed l (coalesced).  tmp: k doubles.
+__device__ void trtri_lower_device(double* S, int ld, int k, double* tmp) {
   const int tid = threadIdx.x;
-  for (int j = 0; j < k; ++j) {
+  for (int j = k - 1; j >= 0; --j) {
     const double ajj = 1.0 / S[(size_t)j * ld + j];
-    for (int i = tid; i < j; i += CHOL_NT) tmp[i] = S[(size_t)j * ld + i];
+    for (int l = j + 1 + tid; l < k; l += CHOL_NT) tmp[l] = S[(size_t)j * ld + l];
     __syncthreads();
-    // column j (rows < j) = -ajj * Rinv[0:j, 0:j] * R[0:j, j]
-    for (int i = tid; i < j; i += CHOL_NT) {
-      double s = 0.0;
-      for (int l = i; l < j; ++l) s += S[(size_t)l * ld + i] * tmp[l];
-      S[(size_t)j * ld + i] = -ajj * s;
+    for (int i = j + 1 + tid; i < k; i += CHOL_NT) {
+      double acc = 0.0;
+      for (int l = j + 1; l <= i; ++l) acc += S[(size_t)l * ld + i] * tmp[l];
+      S[(size_t)j * ld + i] = -ajj * acc;
     }
     __syncthreads();
     if (tid == 0) S[(size_t)j * ld + j] = ajj;
     __syncthreads();
   }
 }
+// Batched Cholesky G = R^T R (R = L^T upper) and R^{-1} = (L^{-1})^T, for CholeskyQR2 of the
+// NNCA bases (reading R13) and the null-space basis of R31.  One CTA per matrix, in shared
+// memory up to CHOL_SMEM_MAX, else in global memory (Rinv's storage, in place).
 constexpr int CHOL_SMEM_MAX = 160;
 __global__ void __launch_bounds__(CHOL_NT) chol_inv_kernel(const CholTask* __restrict__ tasks, int smem_doubles) {
   extern __shared__ double csm[];
@@ -779,31 +775,34 @@ __global__ void __launch_bounds__(CHOL_NT) chol_inv_kernel(const CholTask* __res
   if (k == 0) { if (threadIdx.x == 0) *tk.info = 0; return; }
   const bool smem = (long long)k * (k + 1) <= smem_doubles;
   double* S = smem ? csm : tk.Rinv;
-  double* tmp = smem ? csm + (size_t)k * k : tk.R;   // global path: R's storage is the temp until the end
+  double* tmp = smem ? csm + (size_t)k * k : csm;     // k doubles
   for (int c = 0; c < k; ++c)
     for (int r = threadIdx.x; r < k; r += CHOL_NT) S[(size_t)c * k + r] = tk.G[(size_t)c * k + r];
   __syncthreads();
-  const int info = chol_inv_device(S, k, k, tmp);
+  const int info = chol_lower_device(S, k, k);
   if (threadIdx.x == 0) *tk.info = info;
   if (info) return;
+  // R = L^T (upper; zero below the diagonal)
+  for (int c = 0; c < k; ++c)
+    for (int r = threadIdx.x; r < k; r += CHOL_NT) tk.R[(size_t)c * k + r] = (r <= c) ? S[(size_t)r * k + c] : 0.0;
+  __syncthreads();
+  trtri_lower_device(S, k, k, tmp);
+  // R^{-1} = X^T (upper)
   if (smem) {
     for (int c = 0; c < k; ++c)
-      for (int r = threadIdx.x; r < k; r += CHOL_NT) tk.R[(size_t)c * k + r] = S[(size_t)c * k + r];
-    __syncthreads();
-    trtri_upper_device(S, k, k, tmp);
-    for (int c = 0; c < k; ++c)
-      for (int r = threadIdx.x; r < k; r += CHOL_NT) tk.Rinv[(size_t)c * k + r] = S[(size_t)c * k + r];
+      for (int r = threadIdx.x; r < k; r += CHOL_NT) tk.Rinv[(size_t)c * k + r] = (r <= c) ? S[(size_t)r * k + c] : 0.0;
   } else {
-    // R is in Rinv's storage: copy it out, then invert in place using a column of dynamic smem
-    for (int c = 0; c < k; ++c)
-      for (int r = threadIdx.x; r < k; r += CHOL_NT) tk.R[(size_t)c * k + r] = S[(size_t)c * k + r];
+    // in place: the strict upper part is written from the lower part (disjoint), then zeroed below
+    for (int c = 1; c < k; ++c)
+      for (int r = threadIdx.x; r < c; r += CHOL_NT) S[(size_t)c * k + r] = S[(size_t)r * k + c];
     __syncthreads();
-    trtri_upper_device(S, k, k, csm);
+    for (int c = 0; c < k; ++c)
+      for (int r = c + 1 + threadIdx.x; r < k; r += CHOL_NT) S[(size_t)c * k + r] = 0.0;
   }
 }
 void launch_chol_inv(const CholTask* t, int ntasks, int kmax, cudaStream_t s) {
   const int kk = std::min(kmax, CHOL_SMEM_MAX);
-  const int nd = std::max(kk * (kk + 1), kmax);   // global-path tasks need k doubles of temp
+  const int nd = std::max(kk * (kk + 1), kmax);   // global-path tasks need k doubles of smem temp
   ensure_dyn_smem(chol_inv_kernel, (size_t)nd * sizeof(double));
   LAUNCH(chol_inv_kernel, ntasks, CHOL_NT, (size_t)nd * sizeof(double), s, t, nd);
 }
