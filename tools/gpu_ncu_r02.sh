@@ -9,7 +9,7 @@ cap() {  # name, ncu filter args..., kernel regex for the summary
   python tools/ncu_kernel_traffic.py /tmp/prof_$name.ncu-rep gpurun_out/r02_ncu_$name.json "$rx" > /dev/null 2>&1
   cat gpurun_out/r02_ncu_$name.json | head -14
 }
-cap schur "gemm_tasks_kernel" --nvtx --nvtx-include "schur/" --launch-skip 60 -c 12
+cap schur "gemm_tasks_kernel" --nvtx --nvtx-include "schur/" --launch-skip 4 -c 8
 cap hhupdate "hh_update" -k regex:hh_update --launch-skip 400 -c 8
 cap hhpanel "hh_panel" -k regex:hh_panel_cluster_kernel --launch-skip 100 -c 6
 cap pqr "pqr" -k regex:pqr_cluster --launch-skip 10 -c 4
