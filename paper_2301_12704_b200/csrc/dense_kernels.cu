@@ -1808,11 +1808,11 @@ hh_panel_cluster_smem_kernel(const HHTask* __restrict__ tasks, int j, int cap_ro
 // shared memory, the products run on DMMA (mma.sync m8n8k4 f64).  Fixed summation order.
 struct HHUTile { int task, n0; };
 constexpr int HHU_NT = 256;
-constexpr int HHU_BN = 64, HHU_RK = 32;   // column block, row chunk (pipeline stages: template)
+constexpr int HHU_BN = 64;   // column block (row chunk HHU_RK and pipeline stages: template)
 constexpr int HHU_LV = HHB + 4, HHU_LC = HHU_BN + 4;  // padded rows (stride = 4 mod 16: no bank conflicts)
-template <int HHU_ST>
+template <int HHU_ST, int HHU_RK = 32>
 constexpr size_t hhu_smem() { return sizeof(double) * ((size_t)HHU_ST * HHU_RK * (HHU_LV + HHU_LC) + (size_t)HHB * HHU_LC); }
-template <int HHU_ST>
+template <int HHU_ST, int HHU_RK = 32>
 __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restrict__ tasks,
                                                            const HHUTile* __restrict__ tiles, int j) {
   extern __shared__ __align__(16) double hhu_smem[];
@@ -1906,8 +1906,12 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
     issue(ch + HHU_ST - 1);
     cp_async_wait<HHU_ST - 1>();
     __syncthreads();
-    const double* vs = Vs + (size_t)(ch % HHU_ST) * HHU_RK * HHU_LV;
-    double* cs = Cs + (size_t)(ch % HHU_ST) * HHU_RK * HHU_LC;
+    const double* vs0 = Vs + (size_t)(ch % HHU_ST) * HHU_RK * HHU_LV;
+    double* cs0 = Cs + (size_t)(ch % HHU_ST) * HHU_RK * HHU_LC;
+#pragma unroll
+    for (int rb = 0; rb < HHU_RK; rb += 32) {   // 32-row sub-blocks (2 x 4 warps over 32 x 64)
+    const double* vs = vs0 + (size_t)rb * HHU_LV;
+    double* cs = cs0 + (size_t)rb * HHU_LC;
     double o[2][2][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -1931,6 +1935,8 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
       for (int q = 0; q < 2; ++q)
 #pragma unroll
         for (int e = 0; e < 2; ++e) cs[(wm + i * 8 + (lane >> 2)) * HHU_LC + wn + q * 8 + (lane & 3) * 2 + e] -= o[i][q][e];
+    }
+    const double* cs = cs0;
     __syncthreads();
     const int r0 = ch * HHU_RK;
     for (int e = tid; e < HHU_RK * HHU_BN; e += HHU_NT) {
@@ -1943,7 +1949,10 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
 }
 void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s) {
   static const int st = getenv("AIFMM_HHU_ST") ? atoi(getenv("AIFMM_HHU_ST")) : 3;   // experiment toggle
-  if (st == 2) {
+  if (st == 64) {            // 64-row chunks, 2 stages (experiment)
+    ensure_dyn_smem(hh_update_kernel<2, 64>, hhu_smem<2, 64>());
+    LAUNCH((hh_update_kernel<2, 64>), ntiles, HHU_NT, (hhu_smem<2, 64>()), s, static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j);
+  } else if (st == 2) {
     ensure_dyn_smem(hh_update_kernel<2>, hhu_smem<2>());
     LAUNCH(hh_update_kernel<2>, ntiles, HHU_NT, hhu_smem<2>(), s, static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j);
   } else {
