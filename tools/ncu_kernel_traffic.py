@@ -20,11 +20,26 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "nseco
          "ms": 1e3, "msecond": 1e3}
 
 
+def _f(x):
+    try:
+        return float(x.replace(",", ""))
+    except ValueError:
+        return float("nan")
+
+
 def col(name):
+    """values of one metric over the captured launches; launches where ncu could not collect
+    it (n/a, e.g. a launch replayed in fewer passes) are dropped"""
     if name not in h:
         return None
     i = h.index(name)
-    return [float(r[i].replace(",", "")) * SCALE.get(units[i], 1.0) for r in data]
+    v = [_f(r[i]) * SCALE.get(units[i], 1.0) for r in data]
+    v = [x for x in v if x == x]
+    return v or None
+
+
+def mean(v):
+    return sum(v) / len(v) if v else None
 
 
 dur = col("gpu__time_duration.sum")                       # us
@@ -35,17 +50,20 @@ stalls = {}
 for i, k in enumerate(h):
     m = re.match(r"smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio", k)
     if m:
-        stalls[m.group(1)] = sum(float(r[i]) for r in data) / len(data)
+        v = [x for x in (_f(r[i]) for r in data) if x == x]
+        if v:
+            stalls[m.group(1)] = sum(v) / len(v)
 n = len(data)
 summary = {
     "report": rep, "kernel_filter": pat.pattern, "launches_captured": n,
+    "launches_with_dram_metrics": len(rd) if rd else 0,
     "kernel": data[0][h.index("Kernel Name")].split("(")[0] if n else None,
-    "mean_duration_us": sum(dur) / n if n else None,
-    "dram_bytes_per_launch": (sum(rd) + sum(wr)) / n if n and rd and wr else None,
-    "dram_read_bytes_per_launch": sum(rd) / n if n and rd else None,
-    "dram_write_bytes_per_launch": sum(wr) / n if n and wr else None,
-    "dmma_pipe_pct_of_peak_active": sum(dmma) / n if n and dmma else None,
-    "warps_active_pct": sum(occ) / n if n and occ else None,
+    "mean_duration_us": mean(dur),
+    "dram_bytes_per_launch": (mean(rd) + mean(wr)) if rd and wr else None,
+    "dram_read_bytes_per_launch": mean(rd),
+    "dram_write_bytes_per_launch": mean(wr),
+    "dmma_pipe_pct_of_peak_active": mean(dmma),
+    "warps_active_pct": mean(occ),
     "top_stalls_per_issue": dict(sorted(stalls.items(), key=lambda x: -x[1])[:6]),
     "note": "ncu --set full --clock-control none: cold caches, serialised launches (absolute times "
             "are not bench values)",
