@@ -132,3 +132,42 @@ def test_pivot_inverse_cluster_sizes(cl):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [{"AIFMM_SYM_SCHUR": "1"}, {"AIFMM_NULLSPACE": "1"},
+                                 {"AIFMM_SYM_SCHUR": "1", "AIFMM_NULLSPACE": "1"}],
+                         ids=["R30", "R31", "R30+R31"])
+def test_opt_in_elimination_variants(env):
+    """The opt-in elimination variants (read once per process, so each runs in a subprocess):
+    R30 symmetric Schur pairs, R31 null-space pivot inverses with rank-(m-k) Schur terms.  Both
+    are exact in exact arithmetic, so the factorization must agree with the oracle exactly as the
+    default does: solution within 10*tol, residual within 2x, on a ragged 2D log case and a 3D
+    1/r case; and with tol_c = 0 the solve must equal the densified NNCA matrix's."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, %r)\n"
+        "from paper_2301_12704_b200 import aifmm as G, workloads as W\n"
+        "from oracle.factor import AIFMM as Oracle\n"
+        "from oracle import dense\n"
+        "for kind, n, d, kid, kp, leaf, tol in (('uniform_pm1', 3000, 2, 0, (10.0, 0.0), 40, 1e-8),\n"
+        "                                       ('uniform_01', 3000, 3, 2, (100.0, 0.0), 32, 1e-7)):\n"
+        "    pts = W.make_points(kind, n, d, 21); b = W.make_rhs(n, 2, 21)\n"
+        "    xo = Oracle(pts, kid, kp, leaf, tol).factor().solve(b)\n"
+        "    G.free(); G.build(torch.from_numpy(pts).cuda(), kid, kp, leaf, tol); G.factor()\n"
+        "    x = G.solve(torch.from_numpy(b).cuda()).cpu().numpy()\n"
+        "    rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)\n"
+        "    assert rel <= 10 * tol, (kind, rel)\n"
+        "    assert dense.residual(pts, kid, kp, x, b) <= 2 * dense.residual(pts, kid, kp, xo, b) + 1e-13\n"
+        "pts, b = W.small_problem(d=2, n=1500, seed=9)\n"
+        "o = Oracle(pts, 0, (10.0, 0.0), 24, 1e-5, tol_c=0.0)\n"
+        "G.free(); G.set_compression_tol(0.0); G.build(torch.from_numpy(pts).cuda(), 0, (10.0, 0.0), 24, 1e-5); G.factor()\n"
+        "x = G.solve(torch.from_numpy(b).cuda()).cpu().numpy()\n"
+        "xh = np.linalg.solve(dense.h2_matrix(o), b)\n"
+        "assert np.linalg.norm(x - xh) / np.linalg.norm(xh) <= 1e-10\n"
+        "print('ok')\n" % root)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=900, cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
