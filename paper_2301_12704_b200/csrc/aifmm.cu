@@ -278,6 +278,15 @@ struct Ctx {
 
 static Ctx* g_ctx = nullptr;
 static std::string g_err;
+// Reading R32 (symmetric records): with V = U (R27) and a symmetric kernel
+// the column multipliers of an elimination are the transposes of its row multipliers
+// (C_p = R_p^T), so the solve replays C_p through R_p^T and the blocks that would only serve
+// as C records live in the per-level scratch pool instead of the persistent record pool
+// (about half the near-block record memory).  AIFMM_FULL_RECORDS=1 keeps both (debug toggle).
+static bool half_records() {
+  static const bool v = getenv("AIFMM_FULL_RECORDS") == nullptr;
+  return v;
+}
 enum { PH_PIVOT = 0, PH_TRI = 1, PH_PQR = 2, PH_REDIR = 3 };
 // records an event pair around a phase's launches when timing is on
 struct PhaseTimer {
@@ -699,8 +708,9 @@ static void setup_level(Ctx& c, int l) {
     const int* nbl = c.nlist(l, b, &nn_);
     for (int t = 0; t < nn_; ++t) {
       const int q = nbl[t];
-      // the diagonal block is consumed by the pivot; off-diagonal ones are solve records
-      DevPool& bp = (q == b) ? S : c.persist;
+      // the diagonal block is consumed by the pivot; off-diagonal ones are solve records: (b, q)
+      // is an R record of b if b is eliminated first, else only a C record of q (R32: scratch)
+      DevPool& bp = (q == b || (half_records() && c.col[l][q] < c.col[l][b])) ? S : c.persist;
       f.nearb.put_at(b, t) = Blk{bp.d(std::max<size_t>((size_t)m * f.m[q], 1)), std::max(m, 1), m, f.m[q]};
     }
   }
@@ -1729,7 +1739,8 @@ static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
       const Blk& R = f.nearb.at(f.key(i, q));
       r.R.push_back({q, R});
       r.Rkind_y.push_back(f.E[q]);
-      DevPool& bp = f.E[q] ? c.scr(l) : c.persist;
+      // (Z_i, x_q | y_q): final if q is eliminated, else a C record of q (R32: scratch)
+      DevPool& bp = (f.E[q] || half_records()) ? c.scr(l) : c.persist;
       Blk nb_{bp.d(std::max<size_t>((size_t)k * live(f, q), 1)), std::max(k, 1), k, live(f, q)};
       cb.copy(W[a] + (size_t)wq.second * n + m, n, nb_.p, nb_.ld, k, live(f, q));
       fresh.push_back({f.key(i, q), nb_});
@@ -1938,6 +1949,9 @@ static void solve_dev(Ctx& c, double* B, int nrhs) {
           const int nn = r.m + r.k;
           if (at.second < 0) {
             if (r.k) g.add(1.0, w[at.first] + r.m, nn, 0);
+          } else if (half_records()) {   // R32: C_p = R_p^T (same partner order in R and C)
+            const Blk& Rb = r.R[at.second].second;
+            if (r.m) g.term(-1.0, Rb.p, Rb.ld, 1, w[at.first], nn, 0, r.m);
           } else {
             const Blk& Cb = r.C[at.second].second;
             if (r.m) g.term(-1.0, Cb.p, Cb.ld, 0, w[at.first], nn, 0, r.m);
