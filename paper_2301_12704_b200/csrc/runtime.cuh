@@ -755,7 +755,9 @@ inline void run_pqr(const std::vector<PqrTask>& v, Uploader& up, cudaStream_t s)
   // many tasks: one CTA each fills the GPU; few tall tasks: 8-CTA clusters
   int mmax = 0;
   for (const PqrTask& t : v) mmax = std::max(mmax, t.m);
-  static const int mm_lim = getenv("AIFMM_PQR_MANY_MMAX") ? atoi(getenv("AIFMM_PQR_MANY_MMAX")) : 400;   // experiment
+  // one CTA per task also for moderately tall tasks when there are many (700: measured -3% pqr time on
+  // config 3, neutral on config 2); AIFMM_PQR_MANY_MMAX overrides
+  static const int mm_lim = getenv("AIFMM_PQR_MANY_MMAX") ? atoi(getenv("AIFMM_PQR_MANY_MMAX")) : 700;
   const bool many = (int)v.size() >= 2 * 148 || ((int)v.size() >= many_threshold() && mmax <= mm_lim);
   for (const PqrTask& t : v) {
     if (t.m >= 128 && !many) big.push_back(t);
