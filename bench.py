@@ -140,9 +140,11 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sn = SAMPLE_N[args.cfg]
+    # bounded per-step sample: the cpu_baseline sample, halved when many steps are requested so
+    # that the whole --steps K run stays within a few minutes (~8 s per 8192-point step)
+    sn = SAMPLE_N[args.cfg] if args.steps <= 5 else SAMPLE_N[args.cfg] // 2
     times = []
-    for _ in range(args.warmup):          # warm imports / BLAS threads on a tiny instance
+    for _ in range(args.warmup):          # warm up on a tiny instance
         _oracle_sample(cfg, 1024)
     for _ in range(max(1, args.steps)):
         r = _oracle_sample(cfg, sn)
