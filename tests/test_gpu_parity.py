@@ -276,3 +276,32 @@ def test_config3_full_size_parity():
     print(f"config 3: rel solution diff {rel:.3e}, residual {rg:.3e} (oracle {ro:.3e}), final-rank mismatches {mism}")
     assert rg <= 2 * ro, (rg, ro)
     assert rel <= 10 * cfg.tol, (rel, mism)
+
+
+@pytest.mark.parametrize("ci,n", [(4, 32768), (5, 65536)], ids=["cfg4_grid3d_32768", "cfg5_rand3d_65536"])
+def test_reduced_config_parity_against_cpp_oracle(ci, n):
+    """BASELINE configs 4 and 5 at reduced N (config 4: the 32^3 grid instead of 64^3, which does
+    not fit one GPU; config 5: 65536 of its 2^21 points, the AIFMM(1e-3) preconditioner applied
+    to b) with the config's kernel, diagonal, leaf size and tol, against the serial C++ oracle's
+    cached result (tools/oracle_golden.py): NNCA ranks bit-exact, solution within 10*tol of the
+    oracle's, sampled direct-sum residual within 2x."""
+    cfg = W.CONFIGS[ci - 1]
+    g, meta = _golden(f"{cfg.name}_n{n}")
+    pts, b = W.make(cfg, n=n)
+    G.free()
+    G.build(torch.from_numpy(pts).cuda(), cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol)
+    perm, L = G.get_tree(n)
+    assert L == meta["L"]
+    for l in range(2, L + 1):
+        assert np.array_equal(G.get_ranks(l, cfg.d, 0), g[f"nnca_{l}"])
+    G.factor()
+    Bd = torch.from_numpy(np.ascontiguousarray(b)).cuda()
+    X = G.solve(Bd)
+    x = X.cpu().numpy()
+    xo = g["x"]
+    rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)
+    rg = G.residual(X, Bd, W.residual_rows(n, cfg.seed))
+    ro = meta["residual_4096_rows"]
+    print(f"{cfg.name} N={n}: rel solution diff {rel:.3e}, residual {rg:.3e} (oracle {ro:.3e})")
+    assert rg <= 2 * ro, (rg, ro)
+    assert rel <= 10 * cfg.tol, rel
