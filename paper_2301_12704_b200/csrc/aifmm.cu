@@ -1422,15 +1422,24 @@ static void nullspace_pivots(Ctx& c, FLevel& f, const std::vector<int>& cs, cons
   g.run(c.up, c.s, &fp);
   for (auto& e : v) { g.task(e.Y, e.m, e.m, e.p, 1.0); g.term(-1.0, e.U, e.m, 0, e.t1, e.k, 0, e.k); }
   g.run(c.up, c.s, &fp);
-  // CholeskyQR: Y^T Y = R^T R, N = Y R^{-1}, N -= U (U^T N)
-  for (auto& e : v) { g.task(e.Gm, e.p, e.p, e.p, 0.0); g.term(1.0, e.Y, e.m, 1, e.Y, e.m, 0, e.m); }
-  g.run(c.up, c.s, &fp);
+  // N = Y R^{-1} with Y = Q R (Householder on a copy of Y: the batched panels of the RRQR's first
+  // stage, R8b machinery; then the triangular factor inverted by the batched Gauss-Jordan),
+  // then N -= U (U^T N).  (A CholeskyQR pass measured 22% of the config-3 run: its one-CTA
+  // Cholesky of the (m-k)^2 Gram matrices is latency-bound.)
   {
-    std::vector<CholTask> ct;
-    for (size_t x = 0; x < nb; ++x) ct.push_back(CholTask{v[x].Gm, v[x].R1, v[x].R1i, v[x].p, 0, f.dinfo + f.nb + cs[ns[x]]});
-    launch_chol_inv(c.up.put(ct), (int)ct.size(), pmax, c.s);
+    CopyBatch yc;
+    std::vector<TriRootReq> tr;
+    for (auto& e : v) {
+      yc.copy(e.Y, e.m, e.N, e.m, e.m, e.p);   // N's storage holds the destroyed copy
+      tr.push_back(TriRootReq{e.N, e.m, e.m, e.p, e.R1, e.p});   // R1 <- R^T (p x p, lower)
+    }
+    yc.run(c.up, c.s);
+    batched_tri_root(tr, c.work, c.up, c.s, &fp, 0);
+    std::vector<InvReq> inv;
+    for (size_t x = 0; x < nb; ++x) inv.push_back(InvReq{v[x].R1, v[x].p, v[x].p, f.dinfo + f.nb + cs[ns[x]]});
+    batched_inverse(inv, c.work, c.up, c.s, &fp);   // R1 <- R^{-T}
   }
-  for (auto& e : v) { g.task(e.N, e.m, e.m, e.p, 0.0); g.term(1.0, e.Y, e.m, 0, e.R1i, e.p, 0, e.p); }
+  for (auto& e : v) { g.task(e.N, e.m, e.m, e.p, 0.0); g.term(1.0, e.Y, e.m, 0, e.R1, e.p, 1, e.p); }
   g.run(c.up, c.s, &fp);
   for (auto& e : v) { g.task(e.t4, e.k, e.k, e.p, 0.0); g.term(1.0, e.U, e.m, 1, e.N, e.m, 0, e.m); }
   g.run(c.up, c.s, &fp);
