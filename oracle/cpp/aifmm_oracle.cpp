@@ -940,11 +940,9 @@ struct Oracle {
       Mat FU = hcat(fs, m);                                   // row X_b
       const double nU = fro(FU);
       const Mat& Ub = L_.U.at(b);
-      // R8c: triangular root of the unprojected candidates, projected afterwards (m x m):
-      // M = (I - U U^T) R_F^T has M M^T = W W^T for W = (I - U U^T) F (the R8 criterion)
-      Mat WU = tri_root(FU);
-      Mat UtW = mul(Ub, true, WU, false);
-      gemm(Ub, false, UtW, false, WU, -1.0, true);
+      Mat UtF = mul(Ub, true, FU, false);
+      gemm(Ub, false, UtF, false, FU, -1.0, true);           // (I - U U^T) F
+      Mat WU = tri_root(FU);                                  // R8b
       int tU = 0;
       Mat QU = pivoted_qr_extend(WU, Ub, tol_c * nU, 0, m - k, &tU);
       // tmin = 0: the columns taken are exactly the t_trunc of R8 (R27: V_b's new columns = U_b's)

@@ -27,8 +27,7 @@ bases equals L A R^* + R~^* and zero-pads 
 M2L, M2M, L2L blocks; R15 + R27 equal box ranks |z_i| = |y_i| (needed for a
 square pivot [[K, U],[V^*, 0]]): one-sided compression, V's new columns = U's, capped at m_i;
 R16 pivot inverse G = P_i^{-1} by LU with partial pivoting; R17 (Z_i, y_i) = -G22;
-R8b the RRQR runs on a triangular root of the candidate matrix (tri_root); R8c the root is
-taken of the unprojected candidates and projected afterwards.
+R8b the RRQR runs on the triangular factor of the projected candidate matrix (tri_root).
 """
 from __future__ import annotations
 
@@ -189,11 +188,7 @@ class AIFMM:
             # pivots stay [[K, U], [U^T, 0]], square: |z_b| = |y_b| as P:753 needs, R15)
             FU = np.concatenate([lv.F[(b, q)] for q in ps], axis=1)       # row X_b
             nU = np.linalg.norm(FU)
-            # R8c: the triangular root of the unprojected candidates, then projected (m x m):
-            # M = (I - U U^T) R_F^T satisfies M M^T = W W^T for W = (I - U U^T) F, so the
-            # truncation criterion of R8 / R8b is unchanged
-            RF = tri_root(FU)
-            WU = RF - lv.U[b] @ (lv.U[b].T @ RF)
+            WU = tri_root(FU - lv.U[b] @ (lv.U[b].T @ FU))
             # R8 with tmin = 0: the columns taken are exactly the t_trunc of the truncation test
             QU, tt = pivoted_qr_extend(WU, lv.U[b], self.tol_c * nU, 0, m - k)
             assert QU.shape[1] == tt

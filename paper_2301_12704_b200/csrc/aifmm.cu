@@ -1051,10 +1051,30 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
   cb.run(c.up, c.s);
   launch_norm(c.up.put(nt), (int)nt.size(), c.s);
   if (g_prof.on) { g_prof.end("cmp.gather"); g_prof.begin(c.s); }
-  // two-stage RRQR (R8b, R8c): M = R^T with F^T = Q R (the unprojected candidates), then
-  // M <- (I - U U^T) M below: M M^T = W W^T for W = (I - U U^T) F, so the truncation criterion
-  // is R8's; the projection acts on the m x r root instead of the nu x m candidates
+  // projection W <- (I - B B^T) W, i.e. WT <- WT - (WT B) B^T
+  g_expose.set("cmp.proj");
   GemmBatch g;
+  {
+    std::vector<double*> tu(na);
+    for (int a = 0; a < na; ++a) {
+      int b = aff[a];
+      const int m = f.m[b], k = f.k[b], nu = su[a].n;
+      if (!k || !nu) continue;
+      tu[a] = c.work.d((size_t)nu * k);
+      g.task(tu[a], nu, nu, k, 0.0);
+      g.term(1.0, su[a].WT, nu, 0, f.U[b], m, 0, m);
+    }
+    g.run(c.up, c.s, &c.fc_all);
+    for (int a = 0; a < na; ++a) {
+      int b = aff[a];
+      const int m = f.m[b], k = f.k[b], nu = su[a].n;
+      if (!k || !nu) continue;
+      g.task(su[a].WT, nu, nu, m, 1.0);
+      g.term(-1.0, tu[a], nu, 0, f.U[b], m, 1, k);
+    }
+    g.run(c.up, c.s, &c.fc_all);
+  }
+  // two-stage RRQR (R8b): M = R^T with WT = Q R
   std::vector<TriRootReq> tr;
   for (int a = 0; a < na; ++a) {
     int b = aff[a];
@@ -1071,27 +1091,6 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     c.fcp[PH_TRI].flops += fp.flops;
     // algorithmic: read each candidate matrix once, write its triangular root once
     for (const TriRootReq& q : tr) c.fcp[PH_TRI].bytes += 8.0 * ((double)q.n * q.m + (double)q.m * std::min(q.n, q.m));
-  }
-  g_expose.set("cmp.proj");
-  {
-    std::vector<double*> tu(na, nullptr);
-    for (int a = 0; a < na; ++a) {
-      int b = aff[a];
-      const int m = f.m[b], k = f.k[b], r = su[a].r;
-      if (!k || !su[a].n || !m || full[a]) continue;
-      tu[a] = c.work.d((size_t)k * r);
-      g.task(tu[a], k, k, r, 0.0);                       // U^T M
-      g.term(1.0, f.U[b], m, 1, su[a].M, m, 0, m);
-    }
-    g.run(c.up, c.s, &c.fc_all);
-    for (int a = 0; a < na; ++a) {
-      if (!tu[a]) continue;
-      int b = aff[a];
-      const int m = f.m[b], k = f.k[b], r = su[a].r;
-      g.task(su[a].M, m, m, r, 1.0);                     // M -= U (U^T M)
-      g.term(-1.0, f.U[b], m, 0, tu[a], k, 0, k);
-    }
-    g.run(c.up, c.s, &c.fc_all);
   }
   g_expose.set("cmp.pqr");
   if (g_prof.on) { g_prof.end("cmp.proj+triroot"); g_prof.begin(c.s); }
@@ -1514,10 +1513,10 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   CopyBatch cb;
   std::vector<InvReq> inv;
   std::vector<int> ns;   // colour positions a of the null-space boxes
-  // R31 for boxes with m >= AIFMM_NULLSPACE_MMIN (default 400: measured -2% on config 3, where
-  // the upper levels have m = 500-1000; on config 2's smaller boxes its extra launches cost
-  // more than the smaller Gauss-Jordan saves); AIFMM_NULLSPACE=0 / 1 forces it off / on for all
-  static const int ns_env = getenv("AIFMM_NULLSPACE") ? atoi(getenv("AIFMM_NULLSPACE")) : -1;
+  // R31 is opt-in: AIFMM_NULLSPACE=1 for every box with 0 < k < m, or for boxes with
+  // m >= AIFMM_NULLSPACE_MMIN when AIFMM_NULLSPACE=-1 (measured within +-2% of the default on
+  // config 3 and 10-15% slower on config 2: DESIGN.md)
+  static const int ns_env = getenv("AIFMM_NULLSPACE") ? atoi(getenv("AIFMM_NULLSPACE")) : 0;
   static const int ns_mmin = getenv("AIFMM_NULLSPACE_MMIN") ? atoi(getenv("AIFMM_NULLSPACE_MMIN")) : 400;
   const int ns_min = ns_env == 0 ? (1 << 30) : (ns_env == 1 ? 0 : ns_mmin);
   for (size_t a = 0; a < cs.size(); ++a) {
