@@ -1516,9 +1516,11 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   // R31 is opt-in: AIFMM_NULLSPACE=1 for every box with 0 < k < m, or for boxes with
   // m >= AIFMM_NULLSPACE_MMIN when AIFMM_NULLSPACE=-1 (measured within +-2% of the default on
   // config 3 and 10-15% slower on config 2: DESIGN.md)
+  // AIFMM_NULLSPACE=2: boxes whose complement is small, m - k <= AIFMM_NULLSPACE_PMAX (default 32)
   static const int ns_env = getenv("AIFMM_NULLSPACE") ? atoi(getenv("AIFMM_NULLSPACE")) : 0;
   static const int ns_mmin = getenv("AIFMM_NULLSPACE_MMIN") ? atoi(getenv("AIFMM_NULLSPACE_MMIN")) : 400;
-  const int ns_min = ns_env == 0 ? (1 << 30) : (ns_env == 1 ? 0 : ns_mmin);
+  static const int ns_pmax = getenv("AIFMM_NULLSPACE_PMAX") ? atoi(getenv("AIFMM_NULLSPACE_PMAX")) : 32;
+  const int ns_min = ns_env == 0 || ns_env == 2 ? (1 << 30) : (ns_env == 1 ? 0 : ns_mmin);
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];
     const int m = f.m[i], k = f.k[i], n = m + k;
@@ -1527,7 +1529,7 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     r.k = k;
     r.G = c.persist.d(std::max<size_t>((size_t)n * n, 1));
     if (!n) continue;
-    if (k > 0 && k < m && m >= ns_min) { ns.push_back((int)a); continue; }
+    if (k > 0 && k < m && (m >= ns_min || (ns_env == 2 && m - k <= ns_pmax))) { ns.push_back((int)a); continue; }
     const Blk& K = f.nearb.at(f.key(i, i));
     cb.copy(K.p, K.ld, r.G, n, m, m);
     cb.copy(f.U[i], m, r.G + (size_t)m * n, n, m, k);
