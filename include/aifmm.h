@@ -12,8 +12,10 @@
  *   (Remark P:1186-1188): build + factor once, solve many times.
  *
  * Conventions
- *   - One implicit context per process (one process per GPU).  Calls are serialised by
- *     the caller; there is no internal locking.
+ *   - One implicit context per process (one process per GPU), one CUDA stream.  Calls are
+ *     serialised by the caller, including solves of one factorization from several host
+ *     threads (they share the context's workspace); there is no internal locking.  The Python
+ *     binding runs every call on torch's current stream (aifmm_set_stream).
  *   - "device" pointers are CUDA device pointers on the current device; "host" pointers
  *     are ordinary (pageable or pinned) host memory.
  *   - Matrices are column-major.  Points are N x d row-major (point i at points[i*d]).
