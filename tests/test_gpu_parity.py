@@ -305,3 +305,20 @@ def test_reduced_config_parity_against_cpp_oracle(ci, n):
     print(f"{cfg.name} N={n}: rel solution diff {rel:.3e}, residual {rg:.3e} (oracle {ro:.3e})")
     assert rg <= 2 * ro, (rg, ro)
     assert rel <= 10 * cfg.tol, rel
+
+
+def test_factorization_deterministic():
+    """Two factorizations of the same input give bitwise-identical solutions and final ranks:
+    every reduction of the GPU path has a fixed order (no atomics), and the host planning is
+    deterministic."""
+    pts, b = W.small_problem(d=2, n=6000, seed=17, nrhs=2)
+    out = []
+    for _ in range(2):
+        G.free()
+        G.build(torch.from_numpy(pts).cuda(), 1, (1.01, 0.1), 48, 1e-8)
+        G.factor()
+        x = G.solve(torch.from_numpy(b).cuda()).cpu().numpy()
+        perm, L = G.get_tree(6000)
+        out.append((x, [G.get_ranks(l, 2, 1) for l in range(2, L + 1)]))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert all(np.array_equal(a, c) for a, c in zip(out[0][1], out[1][1]))
