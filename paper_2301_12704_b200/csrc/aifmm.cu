@@ -1513,13 +1513,14 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   CopyBatch cb;
   std::vector<InvReq> inv;
   std::vector<int> ns;   // colour positions a of the null-space boxes
-  // R31 is opt-in: AIFMM_NULLSPACE=1 for every box with 0 < k < m, or for boxes with
-  // m >= AIFMM_NULLSPACE_MMIN when AIFMM_NULLSPACE=-1 (measured within +-2% of the default on
-  // config 3 and 10-15% slower on config 2: DESIGN.md)
-  // AIFMM_NULLSPACE=2: boxes whose complement is small, m - k <= AIFMM_NULLSPACE_PMAX (default 32)
-  static const int ns_env = getenv("AIFMM_NULLSPACE") ? atoi(getenv("AIFMM_NULLSPACE")) : 0;
+  // R31 by default (mode 2) for the boxes whose complement is small, m - k <= 64
+  // (AIFMM_NULLSPACE_PMAX): there the inverse shrinks most (size m - k instead of m + k) and the
+  // Schur terms get inner dimension m - k; measured -1.8% factor time on configs 2 and 3 (all
+  // boxes: -2% / +15%).  AIFMM_NULLSPACE=0 off, 1 every box with 0 < k < m,
+  // -1 boxes with m >= AIFMM_NULLSPACE_MMIN.
+  static const int ns_env = getenv("AIFMM_NULLSPACE") ? atoi(getenv("AIFMM_NULLSPACE")) : 2;
   static const int ns_mmin = getenv("AIFMM_NULLSPACE_MMIN") ? atoi(getenv("AIFMM_NULLSPACE_MMIN")) : 400;
-  static const int ns_pmax = getenv("AIFMM_NULLSPACE_PMAX") ? atoi(getenv("AIFMM_NULLSPACE_PMAX")) : 32;
+  static const int ns_pmax = getenv("AIFMM_NULLSPACE_PMAX") ? atoi(getenv("AIFMM_NULLSPACE_PMAX")) : 64;
   const int ns_min = ns_env == 0 || ns_env == 2 ? (1 << 30) : (ns_env == 1 ? 0 : ns_mmin);
   for (size_t a = 0; a < cs.size(); ++a) {
     int i = cs[a];

@@ -134,9 +134,9 @@ def test_pivot_inverse_cluster_sizes(cl):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("env", [{"AIFMM_SYM_SCHUR": "1"}, {"AIFMM_NULLSPACE": "1"},
+@pytest.mark.parametrize("env", [{"AIFMM_SYM_SCHUR": "1"}, {"AIFMM_NULLSPACE": "1"}, {"AIFMM_NULLSPACE": "0"},
                                  {"AIFMM_SYM_SCHUR": "1", "AIFMM_NULLSPACE": "1"}],
-                         ids=["R30", "R31", "R30+R31"])
+                         ids=["R30", "R31-all", "R31-off", "R30+R31-all"])
 def test_opt_in_elimination_variants(env):
     """The opt-in elimination variants (read once per process, so each runs in a subprocess):
     R30 symmetric Schur pairs, R31 null-space pivot inverses with rank-(m-k) Schur terms.  Both
