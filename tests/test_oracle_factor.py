@@ -97,8 +97,8 @@ def test_zero_rhs_and_multi_rhs_columns():
 def test_far_fill_rank_theorem1():
     """Theorem 1: the P2P fill-in between well-separated neighbours of an
     eliminated leaf is numerically low rank.  Every leaf-level P2P block that reaches the
-    compression phase is rank deficient: numerical rank (1e-10 relative) <= 50% of its
-    dimension (measured 47% max; SPEC S:409 suggests 40% for its smaller test)."""
+    compression phase is rank deficient: numerical rank (1e-10 relative) <= 40% of its
+    dimension (SPEC S:409's bound; measured: max 27%, mean 15% on this grid)."""
     ranks = []
 
     class Probe(AIFMM):
@@ -116,7 +116,7 @@ def test_far_fill_rank_theorem1():
     kp = (float(np.sqrt(1000 * 4096)), 0.0)
     Probe(pts, 2, kp, 64, 1e-10).factor()
     assert len(ranks) > 20
-    assert max(r / dim for r, dim in ranks) <= 0.5, sorted(ranks)[-5:]
+    assert max(r / dim for r, dim in ranks) <= 0.4, sorted(ranks)[-5:]
 
 
 def test_algorithm2_compress_on_creation():
@@ -138,3 +138,28 @@ def test_algorithm2_compress_on_creation():
     r3 = dense.residual(pts, kid, kp, o3.solve(b), b)
     r2 = dense.residual(pts, kid, kp, o2.solve(b), b)
     assert r2 < 100 * 1e-8 and r3 < 100 * 1e-8, (r2, r3)
+
+
+def test_tri_root_is_a_root_of_the_candidate_gram_matrix():
+    """Reading R8b (oracle/factor.py: tri_root): M = R^T with W^T = Q R satisfies M M^T = W W^T
+    and range(M) = range(W), so for every left projector P the truncation residual
+    ||(I - P) M||_F equals ||(I - P) W||_F (checked on wide, square and tall W, with rank-deficient
+    W, and with P a random orthogonal projector); M is lower trapezoidal."""
+    from oracle.factor import tri_root
+    rng = np.random.default_rng(4)
+    for m, n, r in ((12, 40, 12), (20, 20, 20), (30, 8, 8), (25, 60, 7)):
+        W = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+        M = tri_root(W)
+        assert M.shape == (m, min(m, n))
+        assert np.allclose(M @ M.T, W @ W.T, rtol=0, atol=1e-12 * np.linalg.norm(W) ** 2)
+        assert np.allclose(np.triu(M, 1), 0.0)
+        Q, _ = np.linalg.qr(rng.standard_normal((m, max(1, m // 3))))
+        P = Q @ Q.T
+        a = np.linalg.norm(M - P @ M)
+        b = np.linalg.norm(W - P @ W)
+        assert abs(a - b) <= 1e-12 * np.linalg.norm(W)
+        # range equality: the projection of W onto range(M)^perp vanishes
+        Um, sm, _ = np.linalg.svd(M, full_matrices=False)
+        Um = Um[:, sm > 1e-10 * sm[0]]
+        assert np.linalg.norm(W - Um @ (Um.T @ W)) <= 1e-10 * np.linalg.norm(W)
+        assert Um.shape[1] == r
