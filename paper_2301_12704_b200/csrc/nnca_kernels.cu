@@ -411,7 +411,12 @@ aca_cluster_kernel(const AcaTask* __restrict__ tasks, const double* __restrict__
 }
 
 void launch_aca(const AcaTask* t, int ntasks, const double* pts, KernelParams kp, double eps, cudaStream_t s) {
-  LAUNCH(aca_kernel, ntasks, ACA_NT, 0, s, t, pts, kp, eps);
+  // experiment toggle: unused dynamic shared memory (KB) per CTA to cap the number of resident
+  // boxes, so that their cross histories (V: k x nF each) stay in L2
+  static const int pad_kb = getenv("AIFMM_ACA_SMEM_KB") ? atoi(getenv("AIFMM_ACA_SMEM_KB")) : 0;
+  const size_t smem = (size_t)pad_kb * 1024;
+  if (smem) ensure_dyn_smem(aca_kernel, smem);
+  LAUNCH(aca_kernel, ntasks, ACA_NT, smem, s, t, pts, kp, eps);
 }
 void launch_aca_cluster(const AcaTask* t, int ntasks, int kmax, const double* pts, KernelParams kp, double eps,
                         cudaStream_t s) {
