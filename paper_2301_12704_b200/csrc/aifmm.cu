@@ -1375,18 +1375,17 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
 // D = N^T K N:
 //   G11 = N D^{-1} N^T,   G12 = U - G11 K U,   G21 = U^T - U^T K G11,
 //   G22 = -U^T K U + U^T K G11 K U
-// (exact; independent of the choice of N).  The only inverse is D, of size m - k instead of
-// m + k; everything else is a DMMA GEMM.  N = Y R^{-1} with Y = (I - U U^T) Omega (Omega a fixed
-// counter-based pseudo-random m x (m-k) matrix) and Y^T Y = R^T R (one CholeskyQR pass: cond(N)
-// = 1 + O(eps cond(Y)^2)), re-projected against U once.  G is written into the record r.G exactly
+// (exact; independent of the choice of N).  The only inverses are D and the triangular factor
+// below, of size m - k instead of m + k; everything else is a DMMA GEMM.  N = Y R^{-1} with
+// Y = (I - U U^T) Omega (Omega a fixed counter-based pseudo-random m x (m-k) matrix) and Y = Q R
+// (Householder), re-projected against U once.  G is written into the record r.G exactly
 // where the explicit inverse went, so the multipliers, new blocks and the solve are unchanged.
 static void nullspace_pivots(Ctx& c, FLevel& f, const std::vector<int>& cs, const std::vector<int>& ns, FlopCounter& fp,
                              SchurPlan& P) {
   const size_t nb = ns.size();
-  struct NS { double *Y, *t1, *Gm, *R1, *R1i, *N, *t4, *KN, *KU, *D, *Y1, *t, *t3; int m, k, p, n; const double* U; Blk K; double* G; };
+  struct NS { double *Y, *t1, *R1, *N, *t4, *KN, *KU, *D, *Y1, *t, *t3; int m, k, p, n; const double* U; Blk K; double* G; };
   std::vector<NS> v(nb);
   std::vector<HashFillTask> hf;
-  int pmax = 1;
   for (size_t x = 0; x < nb; ++x) {
     const int i = cs[ns[x]];
     NS& e = v[x];
@@ -1400,9 +1399,7 @@ static void nullspace_pivots(Ctx& c, FLevel& f, const std::vector<int>& cs, cons
     const size_t mp = (size_t)e.m * e.p, pp = (size_t)e.p * e.p;
     e.Y = c.work.d(mp);
     e.t1 = c.work.d((size_t)e.k * e.p);
-    e.Gm = c.work.d(pp);
     e.R1 = c.work.d(pp);
-    e.R1i = c.work.d(pp);
     e.N = c.work.d(mp);
     e.t4 = c.work.d((size_t)e.k * e.p);
     e.KN = c.work.d(mp);
@@ -1411,7 +1408,6 @@ static void nullspace_pivots(Ctx& c, FLevel& f, const std::vector<int>& cs, cons
     e.Y1 = c.work.d(mp);
     e.t = c.work.d((size_t)e.p * e.k);
     e.t3 = c.work.d((size_t)e.k * e.p);
-    pmax = std::max(pmax, e.p);
     hf.push_back(HashFillTask{e.Y, e.m, e.m, e.p, 0x5EEDull * 0x100000001ull + (unsigned long long)e.m * 7919ull + e.p});
   }
   {
