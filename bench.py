@@ -226,7 +226,8 @@ def run_ours(args, cfg):
     launches = 0.0
     keys = ("schur_ms", "schur_flops", "schur_bytes", "schur_launches", "pivot_ms", "pivot_flops", "pivot_bytes",
             "tri_ms", "tri_flops", "tri_bytes", "pqr_ms", "pqr_bytes", "redir_ms", "redir_flops", "redir_bytes",
-            "factor_flops", "max_rank", "compressions", "device_bytes", "host_syncs")
+            "factor_flops", "max_rank", "compressions", "device_bytes", "host_syncs",
+            "mult_ms", "mult_flops", "proj_ms", "proj_flops", "fresh_ms", "fresh_flops", "orth_ms")
     for _ in range(args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
@@ -314,7 +315,14 @@ def run_ours(args, cfg):
                         acc["pqr_bytes"] / K, acc["pqr_ms"] / K, hbm, "GB/s"),
         _phase_roofline("redirection (P:877-882, P:1010-1014, P:1078-1082)", "gemm_tasks_kernel", "hbm",
                         acc["redir_bytes"] / K, acc["redir_ms"] / K, hbm, "GB/s"),
+        _phase_roofline("multipliers W_i = G_i[:, :m] R_i (P:753)", "gemm_tasks_kernel", "tensor",
+                        acc["mult_flops"] / K, acc["mult_ms"] / K, fp64, "TFLOP/s"),
+        _phase_roofline("compression projections (I - U U^T) F (P:841-849, R8)", "gemm_tasks_kernel", "tensor",
+                        acc["proj_flops"] / K, acc["proj_ms"] / K, fp64, "TFLOP/s"),
+        _phase_roofline("new blocks C_p G12, G21 R_q, -G22 (Table 4 P:649-677)", "gemm_tasks_kernel + copy_tasks_kernel",
+                        "tensor", acc["fresh_flops"] / K, acc["fresh_ms"] / K, fp64, "TFLOP/s"),
     ]
+    phase_ms = {k: acc[k + "_ms"] / K for k in ("schur", "pivot", "tri", "pqr", "redir", "mult", "proj", "fresh", "orth")}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         sn = SAMPLE_N[args.cfg]
@@ -330,6 +338,7 @@ def run_ours(args, cfg):
         "config": _config_dict(cfg, parallelism="1 GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
                                l2="flushed (256 MB write) between steps; working set > L2"),
         "phase_ms": {"build": tb / K, "factor": tf / K, "solve": ts / K},
+        "factor_phase_device_ms": phase_ms,
         "rel_residual_4096_rows": res,
         "factor_tflop_per_step": acc["factor_flops"] / K / 1e12,
         "max_rank": acc["max_rank"] / K, "compressions_per_step": acc["compressions"] / K,

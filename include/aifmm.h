@@ -148,7 +148,7 @@ int aifmm_gmres(const double* b, double* x, int restart, double rtol, int maxit,
 int aifmm_residual(const double* X, const double* B, int nrhs, const int64_t* rows, int64_t nrows, double* rel);
 
 /* aifmm_stats — host double[AIFMM_NSTATS], see the AIFMM_STAT_* indices. */
-#define AIFMM_NSTATS 28
+#define AIFMM_NSTATS 40
 #define AIFMM_STAT_BUILD_MS        0
 #define AIFMM_STAT_FACTOR_MS       1
 #define AIFMM_STAT_SOLVE_MS        2
@@ -181,6 +181,21 @@ int aifmm_residual(const double* X, const double* B, int nrhs, const int64_t* ro
 #define AIFMM_STAT_REDIR_MS       25
 #define AIFMM_STAT_REDIR_FLOPS    26
 #define AIFMM_STAT_REDIR_BYTES    27
+/* multipliers W_i = G_i[:, 0:m] R_i, compression projections (I - U U^T) F, the new blocks
+ * of an elimination (C_p G12, G21 R_q, -G22), the level-start orthonormalisation (R13)
+ * (device time includes host planning gaps inside the phase) */
+#define AIFMM_STAT_MULT_MS        28
+#define AIFMM_STAT_MULT_FLOPS     29
+#define AIFMM_STAT_MULT_BYTES     30
+#define AIFMM_STAT_PROJ_MS        31
+#define AIFMM_STAT_PROJ_FLOPS     32
+#define AIFMM_STAT_PROJ_BYTES     33
+#define AIFMM_STAT_FRESH_MS       34
+#define AIFMM_STAT_FRESH_FLOPS    35
+#define AIFMM_STAT_FRESH_BYTES    36
+#define AIFMM_STAT_ORTH_MS        37
+#define AIFMM_STAT_ORTH_FLOPS     38
+#define AIFMM_STAT_ORTH_BYTES     39
 int aifmm_stats(double* out);
 /* aifmm_reset_counters — zero the launch / FLOP / time counters. */
 int aifmm_reset_counters(void);

@@ -28,7 +28,9 @@ STAT_NAMES = ["build_ms", "factor_ms", "solve_ms", "levels", "top_size", "factor
               "schur_flops", "schur_ms", "launches", "compressions", "max_rank", "device_bytes",
               "schur_bytes", "schur_launches", "solve_bytes", "host_syncs",
               "pivot_ms", "pivot_flops", "pivot_bytes", "tri_ms", "tri_flops", "tri_bytes",
-              "pqr_ms", "pqr_flops", "pqr_bytes", "redir_ms", "redir_flops", "redir_bytes"]
+              "pqr_ms", "pqr_flops", "pqr_bytes", "redir_ms", "redir_flops", "redir_bytes",
+              "mult_ms", "mult_flops", "mult_bytes", "proj_ms", "proj_flops", "proj_bytes",
+              "fresh_ms", "fresh_flops", "fresh_bytes", "orth_ms", "orth_flops", "orth_bytes"]
 
 
 class AIFMMError(RuntimeError):

@@ -253,8 +253,8 @@ struct Ctx {
   // per-phase device time (CUDA events bracketing the phase's launches on c.s) and algorithmic
   // work, for the bench's roofline entries: PH_PIVOT pivot factorisations, PH_TRI Householder
   // first stage of the RRQR, PH_PQR truncated pivoted QR, PH_REDIR redirection GEMMs
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evp[4];
-  FlopCounter fcp[4];
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evp[8];
+  FlopCounter fcp[8];
   // accessors
   bool nonempty(int l, int b) const { return off[l][b + 1] > off[l][b]; }
   int count(int l, int b) const { return (int)(off[l][b + 1] - off[l][b]); }
@@ -287,7 +287,7 @@ static bool half_records() {
   static const bool v = getenv("AIFMM_FULL_RECORDS") == nullptr;
   return v;
 }
-enum { PH_PIVOT = 0, PH_TRI = 1, PH_PQR = 2, PH_REDIR = 3 };
+enum { PH_PIVOT = 0, PH_TRI = 1, PH_PQR = 2, PH_REDIR = 3, PH_MULT = 4, PH_PROJ = 5, PH_FRESH = 6, PH_ORTH = 7, NPH = 8 };
 // records an event pair around a phase's launches when timing is on
 struct PhaseTimer {
   Ctx& c;
@@ -1055,6 +1055,7 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
   g_expose.set("cmp.proj");
   GemmBatch g;
   {
+    PhaseTimer pt(c, PH_PROJ);
     std::vector<double*> tu(na);
     for (int a = 0; a < na; ++a) {
       int b = aff[a];
@@ -1064,7 +1065,13 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
       g.task(tu[a], nu, nu, k, 0.0);
       g.term(1.0, su[a].WT, nu, 0, f.U[b], m, 0, m);
     }
-    g.run(c.up, c.s, &c.fc_all);
+    {
+      FlopCounter fp;
+      g.run(c.up, c.s, &fp);
+      c.fc_all.flops += fp.flops;
+      c.fcp[PH_PROJ].flops += fp.flops;
+      c.fcp[PH_PROJ].bytes += fp.bytes;
+    }
     for (int a = 0; a < na; ++a) {
       int b = aff[a];
       const int m = f.m[b], k = f.k[b], nu = su[a].n;
@@ -1072,7 +1079,11 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
       g.task(su[a].WT, nu, nu, m, 1.0);
       g.term(-1.0, tu[a], nu, 0, f.U[b], m, 1, k);
     }
-    g.run(c.up, c.s, &c.fc_all);
+    FlopCounter fp;
+    g.run(c.up, c.s, &fp);
+    c.fc_all.flops += fp.flops;
+    c.fcp[PH_PROJ].flops += fp.flops;
+    c.fcp[PH_PROJ].bytes += fp.bytes;
   }
   // two-stage RRQR (R8b): M = R^T with WT = Q R
   std::vector<TriRootReq> tr;
@@ -1615,7 +1626,14 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
       }
     }
   }
-  g.run(c.up, c.s, &c.fc_all);
+  {
+    PhaseTimer pt(c, PH_MULT);
+    FlopCounter fp;
+    g.run(c.up, c.s, &fp);
+    c.fc_all.flops += fp.flops;
+    c.fcp[PH_MULT].flops += fp.flops;
+    c.fcp[PH_MULT].bytes += fp.bytes;
+  }
   P.W = std::move(W);
   if (g_prof.on) g_prof.end("elim.W");
 }
@@ -1763,8 +1781,15 @@ static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     fresh.push_back({f.key(i, i), nb_});
   }
   g_prof.hlap("fresh");
-  gf.run(c.up, c.s, &c.fc_all);
-  cb.run(c.up, c.s);
+  {
+    PhaseTimer pt(c, PH_FRESH);
+    FlopCounter fp;
+    gf.run(c.up, c.s, &fp);
+    cb.run(c.up, c.s);
+    c.fc_all.flops += fp.flops;
+    c.fcp[PH_FRESH].flops += fp.flops;
+    c.fcp[PH_FRESH].bytes += fp.bytes;
+  }
   if (g_prof.on) { g_prof.end("elim.fresh"); g_prof.begin(c.s); }
   for (auto& fr : fresh) f.nearb[fr.first] = fr.second;
   for (int i : cs) f.E[i] = 1;
@@ -1813,7 +1838,10 @@ static void factor_levels(Ctx& c) {
     FLevel& f = c.fl[l];
     g_prof.end("setup");
     g_prof.begin(c.s);
-    orthonormalise(c, f);
+    {
+      PhaseTimer pt(c, PH_ORTH);
+      orthonormalise(c, f);
+    }
     g_prof.end("orth");
     if (getenv("AIFMM_DEBUG_SYM")) dbg_symmetry(c, f, "after setup");
     int ncol = 0;
@@ -2445,7 +2473,7 @@ int aifmm_factor(void) {
     cudaEventDestroy(e.second);
   }
   c.ev.clear();
-  for (int ph = 0; ph < 4; ++ph) {
+  for (int ph = 0; ph < NPH; ++ph) {
     double t = 0.0;
     for (auto& e : c.evp[ph]) {
       float ms = 0.f;

@@ -20,4 +20,5 @@ for rep in range(2):
     res = A.residual(X, B, rows)
     print(json.dumps({"cfg": cfg.name, "n": len(pts), "build_s": t1-t0, "factor_s": t2-t1, "solve_s": t3-t2, "residual": res,
                       **{k: st[k] for k in ("levels","top_size","max_rank","launches","host_syncs","compressions","schur_flops",
-                                            "factor_flops","device_bytes","schur_ms","pivot_ms","tri_ms","pqr_ms","redir_ms")}}), flush=True)
+                                            "factor_flops","device_bytes","schur_ms","pivot_ms","tri_ms","pqr_ms","redir_ms",
+                                            "mult_ms","proj_ms","fresh_ms","orth_ms")}}), flush=True)
