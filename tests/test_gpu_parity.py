@@ -182,6 +182,12 @@ def test_config2_full_size_parity():
     # max(10*tol, 1.5 * floor).  Configs 1 and 3 and the small cases keep the plain 10*tol.
     g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg2_oracle_rounding_floor.json")))
     floor = g["same_decisions_rel_solution_diff"]
+    # final ranks are reported, not gated: the oracle against itself (same decisions replayed vs
+    # free decisions, exact-arithmetic-equivalent rounding) already differs in ~110 boxes
+    mism = {l: int(sum(1 for bx in o.levels[l].boxes if G.get_ranks(l, 2, 1)[bx] != o.levels[l].k[bx]))
+            for l in o.levels}
+    print(f"config 2: rel solution diff {rel:.3e} (floor {floor:.2e}), residual {rg:.3e} (oracle {ro:.3e}), "
+          f"final-rank mismatches {mism} (oracle vs itself: {g['free_decisions_rank_mismatches']})")
     assert rel <= max(10 * cfg.tol, 1.5 * floor), (rel, floor)
 
 
