@@ -184,8 +184,8 @@ def test_config2_full_size_parity():
     floor = g["same_decisions_rel_solution_diff"]
     # final ranks are reported, not gated: the oracle against itself (same decisions replayed vs
     # free decisions, exact-arithmetic-equivalent rounding) already differs in ~110 boxes
-    mism = {l: int(sum(1 for bx in o.levels[l].boxes if G.get_ranks(l, 2, 1)[bx] != o.levels[l].k[bx]))
-            for l in o.levels}
+    gr = {l: G.get_ranks(l, 2, 1) for l in o.levels}
+    mism = {l: int(sum(1 for bx in o.levels[l].boxes if gr[l][bx] != o.levels[l].k[bx])) for l in o.levels}
     print(f"config 2: rel solution diff {rel:.3e} (floor {floor:.2e}), residual {rg:.3e} (oracle {ro:.3e}), "
           f"final-rank mismatches {mism} (oracle vs itself: {g['free_decisions_rank_mismatches']})")
     assert rel <= max(10 * cfg.tol, 1.5 * floor), (rel, floor)
