@@ -808,18 +808,20 @@ static void setup_level(Ctx& c, int l) {
 // once: DMMA GEMMs plus one batched Cholesky; T = R2 R1 so that B_old = Q T.  Returns false if
 // a Gram matrix is not numerically positive definite (then the pivoted-QR path runs instead).
 static bool bases_cholqr2(Ctx& c, FLevel& f, std::vector<double*>& T, std::vector<double*>& T2) {
+  // V_b = U_b bitwise at every level start (R27: V's new columns are copies of U's; R10 at the
+  // leaves; the same operations on Ud and Vd above), so only U is factored: V <- Q, T' = T
   std::vector<int> bx;
   int kmax = 0;
   for (int b : f.boxes)
     if (f.k[b]) { bx.push_back(b); kmax = std::max(kmax, f.k[b]); }
   if (bx.empty()) return true;
-  const int nt = 2 * (int)bx.size();
+  const int nt = (int)bx.size();
   int* dinfo = c.work.i(2 * nt);
   AIFMM_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int) * 2 * nt, c.s));
   std::vector<double*> B(nt), Q1(nt), G(nt), R1(nt), R1i(nt), R2(nt), R2i(nt);
   for (int t = 0; t < nt; ++t) {
-    const int b = bx[t / 2], m = f.m[b], k = f.k[b];
-    B[t] = (t & 1) ? f.V[b] : f.U[b];
+    const int b = bx[t], m = f.m[b], k = f.k[b];
+    B[t] = f.U[b];
     Q1[t] = c.work.d((size_t)m * k);
     G[t] = c.work.d((size_t)k * k);
     R1[t] = c.work.d((size_t)k * k);
@@ -830,20 +832,20 @@ static bool bases_cholqr2(Ctx& c, FLevel& f, std::vector<double*>& T, std::vecto
   auto pass = [&](std::vector<double*>& src, std::vector<double*>& R, std::vector<double*>& Ri, int info0) {
     GemmBatch g;
     for (int t = 0; t < nt; ++t) {
-      const int b = bx[t / 2], m = f.m[b], k = f.k[b];
+      const int b = bx[t], m = f.m[b], k = f.k[b];
       g.task(G[t], k, k, k, 0.0);
       g.term(1.0, src[t], m, 1, src[t], m, 0, m);
     }
     g.run(c.up, c.s, &c.fc_all);
     std::vector<CholTask> ct(nt);
-    for (int t = 0; t < nt; ++t) ct[t] = CholTask{G[t], R[t], Ri[t], f.k[bx[t / 2]], 0, dinfo + info0 + t};
+    for (int t = 0; t < nt; ++t) ct[t] = CholTask{G[t], R[t], Ri[t], f.k[bx[t]], 0, dinfo + info0 + t};
     launch_chol_inv(c.up.put(ct), nt, kmax, c.s);
   };
   pass(B, R1, R1i, 0);
   {
     GemmBatch g;
     for (int t = 0; t < nt; ++t) {
-      const int b = bx[t / 2], m = f.m[b], k = f.k[b];
+      const int b = bx[t], m = f.m[b], k = f.k[b];
       g.task(Q1[t], m, m, k, 0.0);
       g.term(1.0, B[t], m, 0, R1i[t], k, 0, k);
     }
@@ -855,15 +857,18 @@ static bool bases_cholqr2(Ctx& c, FLevel& f, std::vector<double*>& T, std::vecto
     if (v) return false;
   GemmBatch g;
   for (int t = 0; t < nt; ++t) {
-    const int b = bx[t / 2], m = f.m[b], k = f.k[b];
+    const int b = bx[t], m = f.m[b], k = f.k[b];
     double* Tt = c.work.d((size_t)k * k);
-    ((t & 1) ? T2 : T)[b] = Tt;
+    T[b] = T2[b] = Tt;
     g.task(B[t], m, m, k, 0.0);                 // Q = Q1 R2^{-1}
     g.term(1.0, Q1[t], m, 0, R2i[t], k, 0, k);
     g.task(Tt, k, k, k, 0.0);                   // T = R2 R1
     g.term(1.0, R2[t], k, 0, R1[t], k, 0, k);
   }
   g.run(c.up, c.s, &c.fc_all);
+  CopyBatch vc;
+  for (int b : bx) vc.copy(f.U[b], f.m[b], f.V[b], f.m[b], f.m[b], f.k[b]);
+  vc.run(c.up, c.s);
   return true;
 }
 
