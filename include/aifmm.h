@@ -148,7 +148,7 @@ int aifmm_gmres(const double* b, double* x, int restart, double rtol, int maxit,
 int aifmm_residual(const double* X, const double* B, int nrhs, const int64_t* rows, int64_t nrows, double* rel);
 
 /* aifmm_stats — host double[AIFMM_NSTATS], see the AIFMM_STAT_* indices. */
-#define AIFMM_NSTATS 40
+#define AIFMM_NSTATS 42
 #define AIFMM_STAT_BUILD_MS        0
 #define AIFMM_STAT_FACTOR_MS       1
 #define AIFMM_STAT_SOLVE_MS        2
@@ -196,11 +196,54 @@ int aifmm_residual(const double* X, const double* B, int nrhs, const int64_t* ro
 #define AIFMM_STAT_ORTH_MS        37
 #define AIFMM_STAT_ORTH_FLOPS     38
 #define AIFMM_STAT_ORTH_BYTES     39
+/* multi-GPU (aifmm_dist_init): bytes this rank received in ownership exchanges during the
+ * last factorization, and the number of exchanges */
+#define AIFMM_STAT_DIST_BYTES     40
+#define AIFMM_STAT_DIST_EXCHANGES 41
 int aifmm_stats(double* out);
 /* aifmm_reset_counters — zero the launch / FLOP / time counters. */
 int aifmm_reset_counters(void);
 /* aifmm_set_timing — 1: record CUDA events around the Schur launches (for bench roofline). */
 int aifmm_set_timing(int on);
+
+/* ---- the factorization split across ranks (one process per GPU) ------------
+ * The paper's per-level loop (Alg. 3) runs colour by colour; the boxes of one
+ * colour are independent (Remark P:402-404), so their work is split by subtree: the boxes of
+ * the coarse level l_p are cut into `world` contiguous Morton ranges of about equal point
+ * count, and a box below l_p belongs to the rank owning its level-l_p ancestor.
+ * Owner computes, state replicated: every rank builds the same tree / lists / NNCA and holds
+ * every block; in each colour of a level below l_p a rank compresses (RRQR) only
+ * its own boxes, inverts only its own pivots and forms their multipliers, and
+ * performs only the Schur updates (Table 4) of target blocks whose row box it owns;
+ * each of these three phases ends with an exchange that gives every rank the blocks the others
+ * wrote (new basis columns with their ranks, G_i and W_i, updated targets).  Levels <= l_p,
+ * the level set-up, orthonormalisation, redirection, new blocks, top and solve run
+ * redundantly.  Every rank ends with the same factorization and solves locally.  The reading
+ * R31 (null-space pivots) and the opt-in R30 are not used while distributed.
+ *
+ * aifmm_dist_unique_id — host out[128]: a fresh NCCL unique id (call on one rank, send it to
+ *   the others, e.g. with torch.distributed.broadcast_object_list).  Errors: ENCCL.
+ * aifmm_dist_init — join an NCCL communicator of `world` ranks as `rank` (one GPU per rank;
+ *   the current CUDA device must be this rank's).  unique_id: host, 128 bytes from
+ *   aifmm_dist_unique_id.  level_p: the partition level l_p (-1: automatic, the first level
+ *   with at least 4 * world non-empty boxes, and below the leaf level).  Collective: every
+ *   rank calls it, then every rank calls build / factor with the SAME arguments.  A world of 1
+ *   is the single-GPU path.  Errors: EINVALID_ARG, ENCCL.
+ * aifmm_dist_init_local — the same over an in-process transport, for validation on one GPU:
+ *   `world` copies of this library loaded in one process, each driven by its own host thread
+ *   and stream, meet through `shared` (host memory of at least 4096 bytes, zeroed before the
+ *   first init, the same pointer for every rank) and exchange by device-to-device copies.
+ * aifmm_dist_finalize — leave the communicator (back to the single-GPU path).
+ * aifmm_get_owners — host int32[2^(d*level)]: owning rank of every box at `level` of the last
+ *   factorization's partition (-1: computed redundantly, level <= l_p or not distributed).
+ *   Errors: ESTATE before a build.
+ * A rank that raises inside a distributed factorization leaves the others waiting in the next
+ * exchange: errors are fatal for the job (as with any collective). */
+int aifmm_dist_unique_id(void* out);
+int aifmm_dist_init(int rank, int world, const void* unique_id, int level_p);
+int aifmm_dist_init_local(int rank, int world, void* shared, int level_p);
+int aifmm_dist_finalize(void);
+int aifmm_get_owners(int level, int32_t* owner);
 
 /* Test hook: in-place inverse of one n x n column-major device matrix with the library's
  * batched Gauss-Jordan (R16; the kernel behind pivot inverses and the top solve). */

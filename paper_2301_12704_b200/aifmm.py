@@ -6,8 +6,12 @@ built library, or calling it without a CUDA device, raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
+import shutil
+import tempfile
+import threading
 
 import numpy as np
 
@@ -23,14 +27,16 @@ SYMBOLS = ["aifmm_build", "aifmm_set_compression_tol", "aifmm_factor", "aifmm_so
            "aifmm_get_tree", "aifmm_get_level_offsets", "aifmm_get_lists", "aifmm_get_colours",
            "aifmm_get_ranks", "aifmm_stats", "aifmm_reset_counters", "aifmm_set_timing",
            "aifmm_debug_inverse", "aifmm_debug_tri_root", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres",
-           "aifmm_residual", "aifmm_set_algorithm"]
+           "aifmm_residual", "aifmm_set_algorithm", "aifmm_dist_unique_id", "aifmm_dist_init",
+           "aifmm_dist_init_local", "aifmm_dist_finalize", "aifmm_get_owners"]
 STAT_NAMES = ["build_ms", "factor_ms", "solve_ms", "levels", "top_size", "factor_flops",
               "schur_flops", "schur_ms", "launches", "compressions", "max_rank", "device_bytes",
               "schur_bytes", "schur_launches", "solve_bytes", "host_syncs",
               "pivot_ms", "pivot_flops", "pivot_bytes", "tri_ms", "tri_flops", "tri_bytes",
               "pqr_ms", "pqr_flops", "pqr_bytes", "redir_ms", "redir_flops", "redir_bytes",
               "mult_ms", "mult_flops", "mult_bytes", "proj_ms", "proj_flops", "proj_bytes",
-              "fresh_ms", "fresh_flops", "fresh_bytes", "orth_ms", "orth_flops", "orth_bytes"]
+              "fresh_ms", "fresh_flops", "fresh_bytes", "orth_ms", "orth_flops", "orth_bytes",
+              "dist_bytes", "dist_exchanges"]
 
 
 class AIFMMError(RuntimeError):
@@ -40,16 +46,48 @@ class AIFMMError(RuntimeError):
 
 
 _lib = None
+_tls = threading.local()   # per-thread library instance (in-process multi-rank validation)
 
 
 def load(path: str = LIB_PATH):
-    """Load libaifmm.so (raises if it has not been built)."""
+    """Load libaifmm.so (raises if it has not been built).  Inside `use(lib)` the calling
+    thread's instance is returned instead."""
     global _lib
+    inst = getattr(_tls, "lib", None)
+    if inst is not None:
+        return inst
     if _lib is not None:
         return _lib
+    _lib = _open(path)
+    return _lib
+
+
+def load_copy(rank: int):
+    """A separate instance of the library (its own context, pools and stream): a private copy
+    of libaifmm.so loaded RTLD_LOCAL.  Used to run `world` ranks of the distributed
+    factorization in one process on one GPU (aifmm_dist_init_local), one host thread each."""
+    load()
+    d = tempfile.mkdtemp(prefix="aifmm_rank")
+    path = os.path.join(d, f"libaifmm_rank{rank}.so")
+    shutil.copyfile(LIB_PATH, path)
+    return _open(path)
+
+
+@contextlib.contextmanager
+def use(lib):
+    """Route this thread's calls of this module to `lib` (from load_copy)."""
+    old = getattr(_tls, "lib", None)
+    _tls.lib = lib
+    try:
+        yield lib
+    finally:
+        _tls.lib = old
+
+
+def _open(path: str):
     if not os.path.exists(path):
         raise ImportError(f"{path} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
-    lib = ctypes.CDLL(path)
+    lib = ctypes.CDLL(path, mode=os.RTLD_LOCAL | os.RTLD_NOW)
     P, I, D, I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64
     lib.aifmm_build.argtypes = [P, I64, I, I, P, I, D]
     lib.aifmm_set_compression_tol.argtypes = [D]
@@ -73,32 +111,34 @@ def load(path: str = LIB_PATH):
     lib.aifmm_gmres.argtypes = [P, P, I, D, I, I, P, P]
     lib.aifmm_residual.argtypes = [P, P, I, P, I64, P]
     lib.aifmm_set_algorithm.argtypes = [I]
-    _lib = lib
+    lib.aifmm_dist_unique_id.argtypes = [P]
+    lib.aifmm_dist_init.argtypes = [I, I, P, I]
+    lib.aifmm_dist_init_local.argtypes = [I, I, P, I]
+    lib.aifmm_dist_finalize.argtypes = []
+    lib.aifmm_get_owners.argtypes = [I, P]
+    lib.bound_stream = None
     return lib
 
 
 def _check(rc):
     if rc != 0:
-        raise AIFMMError(rc, _lib.aifmm_last_error().decode())
+        raise AIFMMError(rc, load().aifmm_last_error().decode())
 
 
 def _ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-_bound_stream = None
-
-
 def _bind_stream():
     """Run the library on torch's current CUDA stream, so that the tensors this module prepares
     (.to / .contiguous / .clone on that stream) are complete before the library reads them and
     the library's results are ordered before torch's later work (no cross-stream race)."""
-    global _bound_stream
     import torch
+    lib = load()
     s = torch.cuda.current_stream().cuda_stream
-    if s != _bound_stream:
-        _check(load().aifmm_set_stream(ctypes.c_void_p(s)))
-        _bound_stream = s
+    if s != lib.bound_stream:
+        _check(lib.aifmm_set_stream(ctypes.c_void_p(s)))
+        lib.bound_stream = s
 
 
 def build(points, kernel_id: int, kparams, leaf_size: int, tol: float):
@@ -215,9 +255,9 @@ def set_timing(on: bool):
 
 
 def set_stream(stream_ptr: int):
-    global _bound_stream
-    _check(load().aifmm_set_stream(ctypes.c_void_p(stream_ptr)))
-    _bound_stream = stream_ptr
+    lib = load()
+    _check(lib.aifmm_set_stream(ctypes.c_void_p(stream_ptr)))
+    lib.bound_stream = stream_ptr
 
 
 def debug_inverse(M):
@@ -297,3 +337,42 @@ def gmres(b, restart: int = 30, rtol: float = 1e-10, maxit: int = 1000, precond=
     _check(load().aifmm_gmres(ctypes.c_void_p(bc.data_ptr()), ctypes.c_void_p(x.data_ptr()), int(restart), float(rtol),
                               int(maxit), PRECOND[precond], ctypes.byref(it), ctypes.byref(rr)))
     return x, it.value, rr.value
+
+
+# ---------------------------------------------------------------- SURVEY §8(e), multi-GPU
+def dist_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for dist_init; create it on one rank and send it to
+    the others (torch.distributed.broadcast_object_list)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().aifmm_dist_unique_id(buf))
+    return buf.raw
+
+
+def dist_init(rank: int, world: int, unique_id: bytes, level_p: int = -1):
+    """Join the NCCL communicator: the next factorizations split their work by subtree
+    (include/aifmm.h).  Every rank must then call build/factor with the same arguments."""
+    _bind_stream()
+    uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _check(load().aifmm_dist_init(int(rank), int(world), uid, int(level_p)))
+
+
+def local_shared():
+    """Zeroed host rendezvous block for dist_init_local (keep a reference while in use)."""
+    return ctypes.create_string_buffer(4096)
+
+
+def dist_init_local(rank: int, world: int, shared, level_p: int = -1):
+    """In-process transport (validation on one GPU): `world` library instances (load_copy),
+    one host thread each, all passing the same `shared` block."""
+    _bind_stream()
+    _check(load().aifmm_dist_init_local(int(rank), int(world), ctypes.cast(shared, ctypes.c_void_p), int(level_p)))
+
+
+def dist_finalize():
+    _check(load().aifmm_dist_finalize())
+
+
+def get_owners(level: int, d: int):
+    o = np.zeros(1 << (d * level), dtype=np.int32)
+    _check(load().aifmm_get_owners(level, _ptr(o)))
+    return o

@@ -12,7 +12,10 @@ LIB = os.path.join(HERE, "libaifmm.so")
 SOURCES = ["dense_kernels.cu", "tree_kernels.cu", "nnca_kernels.cu", "h2_kernels.cu", "aifmm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr",
+         # private copies of the library (in-process multi-rank validation, tests/test_gpu_dist.py)
+         # must not share function-local statics such as the device chunk cache
+         "-Xcompiler", "-fno-gnu-unique"]
 
 
 def _stale():
@@ -38,7 +41,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     for p, cmd in procs:
         if p.wait() != 0:
             raise subprocess.CalledProcessError(p.returncode, cmd)
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB + ".tmp", "-lcudart"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB + ".tmp", "-lcudart", "-ldl"]
     subprocess.run(cmd, check=True)
     os.replace(LIB + ".tmp", LIB)
     for o in objs:

@@ -20,6 +20,7 @@
 #include <numeric>
 
 #include "runtime.cuh"
+#include "dist.cuh"
 
 namespace aifmm {
 
@@ -255,6 +256,16 @@ struct Ctx {
   // first stage of the RRQR, PH_PQR truncated pivoted QR, PH_REDIR redirection GEMMs
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evp[8];
   FlopCounter fcp[8];
+  // ownership of the boxes of every level (-1: redundant level)
+  Comm comm;
+  int lp_user = -1, lp = -1;
+  std::vector<std::vector<int>> owner;
+  bool dist_level(int l) const { return comm.on() && l > lp && l < (int)owner.size(); }
+  // debug toggle AIFMM_DIST_PHASES: bit 0 compression, 1 pivots, 2 Schur (others redundant)
+  int dist_phases = getenv("AIFMM_DIST_PHASES") ? atoi(getenv("AIFMM_DIST_PHASES")) : 7;
+  bool dist_ph(int l, int bit) const { return dist_level(l) && (dist_phases & bit); }
+  bool mine(int l, int b, int bit = 7) const { return !dist_ph(l, bit) || owner[l][b] == comm.rank; }
+  int own(int l, int b) const { return dist_level(l) ? owner[l][b] : -1; }
   // accessors
   bool nonempty(int l, int b) const { return off[l][b + 1] > off[l][b]; }
   int count(int l, int b) const { return (int)(off[l][b + 1] - off[l][b]); }
@@ -1183,11 +1194,33 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
         ++a1;
       }
       std::vector<int> grp(aff.begin() + a0, aff.begin() + a1), tg;
-      compress_boxes(c, f, grp, part, tg);
-      for (size_t t = 0; t < grp.size(); ++t) tgt[a0 + t] = tg[t];
+      if (c.dist_ph(f.l, 1)) {   // §8(e): a rank compresses its own boxes only
+        std::vector<int> pos_;
+        std::vector<int> mine_;
+        for (size_t t = 0; t < grp.size(); ++t)
+          if (c.mine(f.l, grp[t])) { pos_.push_back((int)t); mine_.push_back(grp[t]); }
+        if (!mine_.empty()) compress_boxes(c, f, mine_, part, tg);
+        for (size_t t = 0; t < pos_.size(); ++t) tgt[a0 + pos_[t]] = tg[t];
+      } else {
+        compress_boxes(c, f, grp, part, tg);
+        for (size_t t = 0; t < grp.size(); ++t) tgt[a0 + t] = tg[t];
+      }
       c.work.reset();
       a0 = a1;
     }
+  }
+  if (c.dist_ph(f.l, 1)) {
+    // the owners' new ranks, then their new basis columns U_b[:, k:k+t] (and V_b's, R27)
+    c.comm.allreduce_int(tgt.data(), na, c.s);
+    std::vector<std::vector<Region>> reg(c.comm.world);
+    for (int a = 0; a < na; ++a) {
+      const int b = aff[a], m = f.m[b], k = f.k[b];
+      if (!tgt[a]) continue;
+      auto& R = reg[c.own(f.l, b)];
+      R.push_back(Region{f.U[b] + (size_t)k * m, m, m, tgt[a]});
+      R.push_back(Region{f.V[b] + (size_t)k * m, m, m, tgt[a]});
+    }
+    c.comm.exchange(reg, c.up, c.s);
   }
   // new ranks
   std::vector<int> grown;
@@ -1283,6 +1316,9 @@ struct SchurPlan {
   std::vector<int> pdim;                    // m - k of a null-space box, 0 otherwise
   std::vector<double*> Nb, Y1b, Rh;         // N (m x p), Y1 (p x m), Rh = Y1 [R_q ...] (p x tot)
   std::vector<std::vector<double*>> Ch;     // C_p N (live_p x p) per neighbour p (order of nbs[a])
+  // §8(e): per task of g, the owner of its target row box and the target block
+  std::vector<int> towner;
+  std::vector<Blk> tblk;
 };
 static int wcol_of(const std::vector<std::pair<int, int>>& w, int q) {
   for (auto& e : w)
@@ -1318,7 +1354,8 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
   std::vector<int> grp_a;
   // R30 is opt-in (AIFMM_SYM_SCHUR=1): half the Schur flops, but measured slower end to end on
   // configs 2 and 3 (the factorisation then takes larger ranks)
-  static const bool no_sym = getenv("AIFMM_SYM_SCHUR") == nullptr;
+  static const bool no_sym_env = getenv("AIFMM_SYM_SCHUR") == nullptr;
+  const bool no_sym = no_sym_env || c.comm.on();   // R30 is not used while distributed
   for (int p = 0; p < f.nb; ++p) {
     if (!isp[p]) continue;
     qa.clear();
@@ -1370,6 +1407,8 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
         P.g.task(nullptr, M, M, N, 0.0);   // temporary T_pq, allocated in eliminate_update
       } else {
         P.g.task(T.p, T.ld, M, N, 1.0);
+        P.towner.push_back(c.own(l, p));
+        P.tblk.push_back(Blk{T.p, T.ld, M, N});
       }
       for (int a : grp_a) {
         const int i = cs[a];
@@ -1518,7 +1557,6 @@ static void nullspace_pivots(Ctx& c, FLevel& f, const std::vector<int>& cs, cons
 static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan& P) {
   g_expose.set("elim.inv");
   const int l = f.l;
-  (void)l;
   if (g_prof.on) g_prof.begin(c.s);
   // 1. G_i = P_i^{-1}, P_i = [[K_ii, U_i],[V_i^T, 0]] (R16).  Boxes with 0 < k < m: null-space
   //    formation (R31, below); the others (k = 0: P = K; k = m, R28): assembled and inverted.
@@ -1542,7 +1580,12 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     r.k = k;
     r.G = c.persist.d(std::max<size_t>((size_t)n * n, 1));
     if (!n) continue;
-    if (k > 0 && k < m && (m >= ns_min || (ns_env == 2 && m - k <= ns_pmax))) { ns.push_back((int)a); continue; }
+    if (!c.mine(l, i, 2)) continue;   // §8(e): G_i arrives from owner(i)
+    // R31 is not used while distributed (its Schur operands live in per-rank temporaries)
+    if (!c.comm.on() && k > 0 && k < m && (m >= ns_min || (ns_env == 2 && m - k <= ns_pmax))) {
+      ns.push_back((int)a);
+      continue;
+    }
     const Blk& K = f.nearb.at(f.key(i, i));
     cb.copy(K.p, K.ld, r.G, n, m, m);
     cb.copy(f.U[i], m, r.G + (size_t)m * n, n, m, k);
@@ -1604,7 +1647,7 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     int i = cs[a];
     const int m = f.m[i], k = f.k[i], n = m + k, pd = P.pdim[a];
     W[a] = c.work.d(std::max<size_t>((size_t)n * P.tot[a], 1));
-    if (!n) continue;
+    if (!n || !c.mine(l, i, 2)) continue;
     if (pd) P.Rh[a] = c.work.d(std::max<size_t>((size_t)pd * P.tot[a], 1));
     for (auto& wq : P.wcol[a]) {
       const int q = wq.first;
@@ -1639,12 +1682,51 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     c.fcp[PH_MULT].flops += fp.flops;
     c.fcp[PH_MULT].bytes += fp.bytes;
   }
+  if (c.dist_ph(l, 2)) {   // §8(e): G_i and W_i from their owners
+    std::vector<std::vector<Region>> reg(c.comm.world);
+    for (size_t a = 0; a < cs.size(); ++a) {
+      const int i = cs[a], n = f.m[i] + f.k[i];
+      if (!n) continue;
+      auto& R = reg[c.own(l, i)];
+      R.push_back(Region{f.rec[i].G, n, n, n});
+      if (P.tot[a]) R.push_back(Region{W[a], n, n, P.tot[a]});
+    }
+    c.comm.exchange(reg, c.up, c.s);
+  }
   P.W = std::move(W);
   if (g_prof.on) g_prof.end("elim.W");
 }
 
 // debug (AIFMM_DEBUG_SYM=1): largest |B_pq - B_qp^T| / max|B_pq| over the near, M2L and pending
 // fill-in blocks of the level (the symmetric system keeps every pair transposed, R27 / R30)
+// debug (AIFMM_DEBUG_DIST=1, distributed runs): FNV digest of the level state (bases, near /
+// M2L / fill-in blocks, records) printed per rank, to find a block an exchange missed
+static void dbg_digest(Ctx& c, FLevel& f, const char* where) {
+  unsigned long long h[5] = {1469598103934665603ull, 1469598103934665603ull, 1469598103934665603ull,
+                             1469598103934665603ull, 1469598103934665603ull};
+  auto eat = [&](int w, const double* p, int ld, int rows, int cols) {
+    if (!p || rows <= 0 || cols <= 0) return;
+    std::vector<double> hb((size_t)ld * (cols - 1) + rows);
+    AIFMM_CUDA(cudaMemcpyAsync(hb.data(), p, sizeof(double) * hb.size(), cudaMemcpyDeviceToHost, c.s));
+    c.up.sync();
+    for (int j = 0; j < cols; ++j)
+      for (int i = 0; i < rows; ++i) {
+        unsigned long long x;
+        std::memcpy(&x, &hb[(size_t)j * ld + i], 8);
+        h[w] = (h[w] ^ x) * 1099511628211ull;
+      }
+  };
+  for (int b : f.boxes) eat(0, f.U[b], f.m[b], f.m[b], f.k[b]);
+  BlkTable* T[3] = {&f.nearb, &f.A, &f.F};
+  for (int w = 0; w < 3; ++w)
+    for (size_t s = 0; s < T[w]->v.size(); ++s)
+      if (T[w]->has[s]) eat(1 + w, T[w]->v[s].p, T[w]->v[s].ld, T[w]->v[s].rows, T[w]->v[s].cols);
+  for (int b : f.boxes)
+    if (f.E[b] && f.rec[b].G) eat(4, f.rec[b].G, f.m[b] + f.k[b], f.rec[b].m + f.rec[b].k, f.rec[b].m + f.rec[b].k);
+  fprintf(stderr, "[dist %d] level %d %s: U %016llx near %016llx M2L %016llx fill %016llx G %016llx\n", c.comm.rank, f.l,
+          where, h[0], h[1], h[2], h[3], h[4]);
+}
+
 static void dbg_symmetry(Ctx& c, FLevel& f, const char* where) {
   double worst[3] = {0, 0, 0};
   int wp[3] = {-1, -1, -1}, wq[3] = {-1, -1, -1};
@@ -1732,7 +1814,20 @@ static void eliminate_update(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
   }
   long long l0 = g_launches;
   nvtxRangePushA("schur");   // lets `ncu --nvtx --nvtx-include schur/` capture exactly these launches
-  P.g.run(c.up, c.s, &c.fc_schur);
+  if (c.dist_ph(l, 4)) {   // §8(e): the targets of my row boxes, then everyone's targets
+    std::vector<char> keep(P.g.size(), 0);
+    std::vector<std::vector<Region>> reg(c.comm.world);
+    for (size_t t = 0; t < P.g.size(); ++t) {
+      keep[t] = P.towner[t] == c.comm.rank;
+      const Blk& T = P.tblk[t];
+      reg[P.towner[t]].push_back(Region{T.p, T.ld, T.rows, T.cols});
+    }
+    GemmBatch mine_ = P.g.filtered(keep);
+    mine_.run(c.up, c.s, &c.fc_schur);
+    c.comm.exchange(reg, c.up, c.s);
+  } else {
+    P.g.run(c.up, c.s, &c.fc_schur);
+  }
   gm.run(c.up, c.s, &c.fc_schur);
   nvtxRangePop();
   c.stats[AIFMM_STAT_SCHUR_LAUNCHES] += (double)(g_launches - l0);
@@ -1812,6 +1907,7 @@ static void deferred_checks(Ctx& c) {
     const FLevel& fl = c.fl[l];
     if (!fl.dinfo) continue;
     std::vector<int> info = d2h(c, fl.dinfo, 2 * (size_t)fl.nb);
+    if (c.dist_level(l)) c.comm.allreduce_int(info.data(), (int)info.size(), c.s);   // owners' flags
     for (int b : fl.boxes)
       if (info[b] || info[fl.nb + b])
         throw Error(AIFMM_ESINGULAR_PIVOT, std::string(info[b] ? "singular pivot" : "null-space basis (R31) not of full rank") +
@@ -1819,9 +1915,42 @@ static void deferred_checks(Ctx& c) {
   }
 }
 
+// §8(e): the boxes of level l_p are cut into world contiguous Morton ranges of about equal point
+// count (the rank of a box is that of its median point); a box below l_p belongs to the owner of
+// its level-l_p ancestor (Morton ids: b >> d (l - l_p)).  Levels <= l_p are redundant.
+static void plan_ownership(Ctx& c) {
+  c.owner.assign(c.L + 1, {});
+  c.lp = -1;
+  if (!c.comm.on()) return;
+  const int W = c.comm.world;
+  int lp = c.lp_user;
+  if (lp < 1) {
+    lp = c.L - 1;
+    for (int l = 2; l < c.L; ++l) {
+      int ne = 0;
+      for (int b = 0; b < (1 << (c.d * l)); ++b) ne += c.nonempty(l, b) ? 1 : 0;
+      if (ne >= 4 * W) { lp = l; break; }
+    }
+  }
+  lp = std::max(1, std::min(lp, c.L - 1));
+  c.lp = lp;
+  std::vector<int> own_p(1 << (c.d * lp), 0);
+  for (size_t b = 0; b < own_p.size(); ++b) {
+    const long long mid = c.off[lp][b] + (c.off[lp][b + 1] - c.off[lp][b]) / 2;
+    own_p[b] = (int)std::min<long long>(W - 1, mid * W / c.n);
+  }
+  for (int l = lp + 1; l <= c.L; ++l) {
+    c.owner[l].assign((size_t)1 << (c.d * l), 0);
+    for (size_t b = 0; b < c.owner[l].size(); ++b) c.owner[l][b] = own_p[b >> (c.d * (l - lp))];
+  }
+}
+
 static void factor_levels(Ctx& c);
 static void factor_all(Ctx& c) {
   g_expose.set("factor.start");
+  plan_ownership(c);
+  c.comm.bytes_in = 0.0;
+  c.comm.exchanges = 0;
   c.fl.assign(c.L + 1, FLevel{});
   AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
   try {
@@ -1861,14 +1990,21 @@ static void factor_levels(Ctx& c) {
       SchurPlan plan;
       plan_schur(c, f, cs, plan);   // host work, overlaps the previous colour's kernels
       g_prof.begin(c.s);
-      if (!S.empty()) compress(c, f, S, [&] { eliminate_invert(c, f, cs, plan); });
+      static const bool dbg_dist = getenv("AIFMM_DEBUG_DIST") != nullptr;
+      if (dbg_dist) dbg_digest(c, f, ("colour " + std::to_string(col) + " start").c_str());
+      if (!S.empty()) compress(c, f, S, [&] {
+          if (dbg_dist) dbg_digest(c, f, ("colour " + std::to_string(col) + " compressed").c_str());
+          eliminate_invert(c, f, cs, plan);
+        });
       else eliminate_invert(c, f, cs, plan);
+      if (dbg_dist) dbg_digest(c, f, ("colour " + std::to_string(col) + " inverted+redirected").c_str());
       g_prof.end(("compress.L" + std::to_string(l)).c_str());
       g_prof.begin(c.s);
       eliminate_update(c, f, cs, plan);
       g_prof.end(("eliminate.L" + std::to_string(l)).c_str());
       static const bool dbg_sym = getenv("AIFMM_DEBUG_SYM") != nullptr;
       if (dbg_sym) dbg_symmetry(c, f, ("after colour " + std::to_string(col)).c_str());
+      if (dbg_dist) dbg_digest(c, f, ("colour " + std::to_string(col) + " eliminated").c_str());
       if (c.algorithm == 2 && !f.pending.empty()) {   // Alg. 2: compress on creation (R29)
         std::vector<std::pair<int, int>> all(f.pending.begin(), f.pending.end());
         compress(c, f, all, [] {});
@@ -2497,6 +2633,8 @@ int aifmm_factor(void) {
   c.stats[AIFMM_STAT_SCHUR_BYTES] = c.fc_schur.bytes;
   c.stats[AIFMM_STAT_FACTOR_FLOPS] = c.fc_all.flops + c.fc_schur.flops;
   c.factored = true;
+  c.stats[AIFMM_STAT_DIST_BYTES] = c.comm.bytes_in;
+  c.stats[AIFMM_STAT_DIST_EXCHANGES] = (double)c.comm.exchanges;
   c.stats[AIFMM_STAT_FACTOR_MS] = ms_since(t0);
   c.stats[AIFMM_STAT_DEVICE_BYTES] =
       (double)chunk_cache().total();
@@ -2742,6 +2880,49 @@ int aifmm_residual(const double* X, const double* B, int nrhs, const int64_t* ro
 int aifmm_set_timing(int on) {
   CAPI_BEGIN
   ctx().timing = on != 0;
+  CAPI_END
+}
+
+// ------------------------------------------------------------------ SURVEY §8(e) (dist.cuh)
+int aifmm_dist_unique_id(void* out) {
+  CAPI_BEGIN
+  AIFMM_REQUIRE(out, AIFMM_EINVALID_ARG, "null pointer");
+  Comm::unique_id(out);
+  CAPI_END
+}
+
+int aifmm_dist_init(int rank, int world, const void* unique_id, int level_p) {
+  CAPI_BEGIN
+  AIFMM_REQUIRE(world >= 1 && rank >= 0 && rank < world && unique_id, AIFMM_EINVALID_ARG, "bad rank/world/unique id");
+  Ctx& c = ctx();
+  c.lp_user = level_p;
+  if (world == 1) c.comm.finalize();
+  else c.comm.init_nccl(rank, world, unique_id, c.s);
+  CAPI_END
+}
+
+int aifmm_dist_init_local(int rank, int world, void* shared, int level_p) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  c.lp_user = level_p;
+  c.comm.init_local(rank, world, shared);
+  CAPI_END
+}
+
+int aifmm_dist_finalize(void) {
+  CAPI_BEGIN
+  ctx().comm.finalize();
+  CAPI_END
+}
+
+int aifmm_get_owners(int level, int32_t* owner) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built, AIFMM_ESTATE, "owners before build");
+  AIFMM_REQUIRE(owner && level >= 0 && level <= c.L, AIFMM_EINVALID_ARG, "bad level");
+  const size_t nb = (size_t)1 << (c.d * level);
+  const bool have = level < (int)c.owner.size() && c.owner[level].size() == nb && c.dist_level(level);
+  for (size_t b = 0; b < nb; ++b) owner[b] = have ? c.owner[level][b] : -1;
   CAPI_END
 }
 

@@ -371,6 +371,22 @@ class GemmBatch {
     terms_.insert(terms_.end(), o.terms_.begin(), o.terms_.end());
   }
   GemmTerm& term_ref(size_t i) { return terms_[i]; }
+  // the tasks with keep[t] != 0, with their terms, in the same order (a rank runs
+  // the tasks it owns; each task's arithmetic is unchanged)
+  GemmBatch filtered(const std::vector<char>& keep) const {
+    GemmBatch o;
+    o.splitk_ = splitk_;
+    for (size_t t = 0; t < tasks_.size(); ++t) {
+      if (!keep[t]) continue;
+      GemmTask k = tasks_[t];
+      const int b = (int)o.terms_.size();
+      o.terms_.insert(o.terms_.end(), terms_.begin() + k.term_begin, terms_.begin() + k.term_end);
+      k.term_begin = b;
+      k.term_end = (int)o.terms_.size();
+      o.tasks_.push_back(k);
+    }
+    return o;
+  }
   GemmTask& task_ref(size_t i) { return tasks_[i]; }
   // Deterministic split-K: single-term tasks with a long K and few output tiles are split into
   // S partial GEMMs into workspace slices, then reduced in a fixed order by a second launch.

@@ -65,3 +65,17 @@ def _load_elsewhere(path):
         binding.load(path)
     finally:
         binding._lib = saved
+
+
+def test_private_copies_share_no_state():
+    """The in-process multi-rank validation (tests/test_gpu_dist.py) loads private copies of the
+    library: no STB_GNU_UNIQUE symbol (function-local statics such as the device chunk cache)
+    may be merged across copies, and NCCL is resolved at run time (no link dependency)."""
+    from paper_2301_12704_b200.build import build_library
+    lib = build_library()
+    out = subprocess.run(["nm", "-D", lib], capture_output=True, text=True, check=True).stdout
+    assert not re.search(r" u ", out), "GNU_UNIQUE symbols present (build without -fno-gnu-unique?)"
+    ldd = subprocess.run(["ldd", lib], capture_output=True, text=True).stdout
+    assert "nccl" not in ldd
+    a, b = binding.load(), binding.load_copy(0)
+    assert a is not b and hasattr(b, "aifmm_dist_init_local")

@@ -1,0 +1,145 @@
+"""SURVEY §8(e) on one GPU: the distributed factorization (owner computes, replicated state;
+include/aifmm.h "aifmm_dist_init") run with `world` ranks in ONE process: each rank
+is a private copy of libaifmm.so (its own context, pools and stream) driven by its own host
+thread, and the ranks exchange through the in-process transport (host rendezvous + device
+copies; no kernel waits on another rank).  The NCCL transport differs only in the three
+collective calls of Comm::exchange / allreduce_int.
+
+Checks: every rank ends with the same factorization (solutions bitwise identical across
+ranks, same final ranks), the work really was split (owners cover the levels below l_p, every
+rank owns boxes, exchanges happened), and the result meets the north_star bars against the
+oracle (solution within 10 tol, residual within 2x)."""
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import dense                      # noqa: E402
+from oracle.factor import AIFMM as Oracle     # noqa: E402
+from paper_2301_12704_b200 import aifmm as G  # noqa: E402
+from paper_2301_12704_b200 import workloads as W  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    G.load()
+    yield
+
+
+_LIBS = {}
+
+
+def _lib(rank):
+    if rank not in _LIBS:
+        _LIBS[rank] = G.load_copy(rank)
+    return _LIBS[rank]
+
+
+def _run_ranks(world, pts, b, kid, kp, leaf, tol, level_p=-1, algorithm=3):
+    shared = G.local_shared()
+    out, errs = {}, []
+    L_holder = {}
+
+    def body(rank):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s), G.use(_lib(rank)):
+                G.free()
+                G.set_algorithm(algorithm)
+                G.dist_init_local(rank, world, shared, level_p)
+                G.build(torch.from_numpy(pts).cuda(), kid, kp, leaf, tol)
+                G.factor()
+                x = G.solve(torch.from_numpy(np.ascontiguousarray(b)).cuda()).cpu().numpy()
+                _, L = G.get_tree(pts.shape[0])
+                L_holder[rank] = L
+                d = pts.shape[1]
+                out[rank] = dict(x=x, stats=G.stats(),
+                                 owners={l: G.get_owners(l, d) for l in range(2, L + 1)},
+                                 ranks={l: G.get_ranks(l, d, 1) for l in range(2, L + 1)})
+                G.dist_finalize()
+                G.set_algorithm(3)
+                G.free()
+                s.synchronize()
+        except Exception as e:   # noqa: BLE001
+            errs.append((rank, repr(e)))
+
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    assert all(not t.is_alive() for t in th), "a rank hung"
+    return out
+
+
+CASES = [
+    # name, kind, n, d, kid, kparams, leaf, tol, nrhs, world, level_p
+    ("2d_log_w2", "uniform_pm1", 12000, 2, 0, (10.0, 0.0), 32, 1e-8, 2, 2, -1),
+    ("2d_matern_w3_lp3", "uniform_pm1", 12000, 2, 1, (1.01, 0.1), 32, 1e-8, 1, 3, 3),
+    ("3d_invr_w2", "uniform_01", 8000, 3, 2, (100.0, 0.0), 32, 1e-6, 1, 2, -1),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_distributed_factorization_in_process(case):
+    name, kind, n, d, kid, kp, leaf, tol, nrhs, world, lp = case
+    pts = W.make_points(kind, n, d, 60)
+    b = W.make_rhs(n, nrhs, 60)
+    out = _run_ranks(world, pts, b, kid, kp, leaf, tol, lp)
+    x0 = out[0]["x"]
+    for r in range(1, world):
+        assert np.array_equal(out[r]["x"], x0), f"rank {r} holds a different factorization"
+        for l in out[0]["ranks"]:
+            assert np.array_equal(out[r]["ranks"][l], out[0]["ranks"][l])
+            assert np.array_equal(out[r]["owners"][l], out[0]["owners"][l])
+    # the work was split: some level below l_p is owned, every rank owns boxes there
+    split = [l for l, o in out[0]["owners"].items() if (o >= 0).any()]
+    assert split, "no distributed level"
+    leafo = out[0]["owners"][max(out[0]["owners"])]
+    assert set(np.unique(leafo[leafo >= 0]).tolist()) == set(range(world))
+    for r in range(world):
+        st = out[r]["stats"]
+        assert st["dist_exchanges"] > 0 and st["dist_bytes"] > 0
+    # north_star bars against the oracle
+    o = Oracle(pts, kid, kp, leaf, tol).factor()
+    xo = o.solve(b)
+    rel = np.linalg.norm(x0 - xo) / np.linalg.norm(xo)
+    assert rel <= 10 * tol, rel
+    rg = dense.residual(pts, kid, kp, x0.reshape(n, -1), b.reshape(n, -1))
+    ro = dense.residual(pts, kid, kp, xo.reshape(n, -1), b.reshape(n, -1))
+    assert rg <= 2 * ro + 1e-13, (rg, ro)
+    print(f"{name}: world {world}, split levels {split}, rel diff vs oracle {rel:.2e}, residual {rg:.2e} "
+          f"(oracle {ro:.2e}), exchanged {out[0]['stats']['dist_bytes'] / 1e6:.1f} MB in "
+          f"{int(out[0]['stats']['dist_exchanges'])} exchanges")
+
+
+def test_distributed_algorithm2_in_process():
+    """Algorithm 2 (compress on creation) through the same ownership split."""
+    pts = W.make_points("uniform_pm1", 6000, 2, 61)
+    b = W.make_rhs(6000, 1, 61)
+    out = _run_ranks(2, pts, b, 0, (10.0, 0.0), 32, 1e-8, -1, algorithm=2)
+    assert np.array_equal(out[0]["x"], out[1]["x"])
+    o = Oracle(pts, 0, (10.0, 0.0), 32, 1e-8, algorithm=2).factor()
+    xo = o.solve(b)
+    assert np.linalg.norm(out[0]["x"] - xo) / np.linalg.norm(xo) <= 1e-7
+
+
+def test_world_one_is_the_single_gpu_path():
+    """dist_init_local with world 1 is the single-GPU path: bitwise the same solution."""
+    pts = W.make_points("uniform_pm1", 5000, 2, 62)
+    b = W.make_rhs(5000, 1, 62)
+    out = _run_ranks(1, pts, b, 0, (10.0, 0.0), 32, 1e-8)
+    G.free()
+    G.build(torch.from_numpy(pts).cuda(), 0, (10.0, 0.0), 32, 1e-8)
+    G.factor()
+    x = G.solve(torch.from_numpy(b).cuda()).cpu().numpy()
+    G.free()
+    assert np.array_equal(out[0]["x"], x)
+    assert out[0]["stats"]["dist_exchanges"] == 0
