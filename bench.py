@@ -8,8 +8,10 @@ and aifmm_solve (Alg. 4).  Inputs are resident in HBM when the timed region star
 (126 MB) is flushed by writing a 256 MB buffer between steps (the step's working set is
 ~160 GB anyway).  `--cfg 2` selects BASELINE config 2 (N = 65,536, log r, 16 RHS).
 
-N>1 (torchrun): every rank factors its own independent instance of the workload (rank-offset
-seed; weak scaling, no data-path collective).
+N>1 (torchrun): the SAME workload factored by all ranks together:
+the tree is split by subtrees at a coarse level, each rank compresses, inverts and updates the
+blocks of its own subtrees and the ranks exchange the results over NCCL after every phase
+(aifmm_dist_init); strong scaling, value = N / (max over ranks of factor + solve time).
 
 --impl reference: the serial C++ oracle (oracle/cpp, one thread) on a bounded sample of the same
 workload (the first 16384 points of the same draw), timed on the host (rank 0 only).
@@ -154,7 +156,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean([t["build_s"] + t["factor_s"] + t["solve_s"] for t in times])),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(cfg, sample_n=sn),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cores(), "kind": "oracle",
                          "sample": f"serial C++ oracle (oracle/cpp) on the first {sn} points of the {cfg.name} draw "
@@ -181,18 +183,19 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     A.load()
     A.set_stream(stream.cuda_stream)
 
-    # N > 1: every rank factors its own independent instance of the workload (same
-    # distribution, kernel, leaf size, tol, nrhs; rank-offset seed): independent replicas, no
-    # data-path collective
-    cfg_r = D.instance_config(cfg, rank)
+    # N > 1: all ranks factor the same workload together (subtree split, NCCL exchanges inside
+    # the library): rank 0 creates the library's NCCL id, the others receive it
+    if world > 1:
+        A.dist_init(rank, world, D.share_unique_id(A.dist_unique_id() if rank == 0 else None))
+    cfg_r = cfg
     pts, b = W.make(cfg_r)
     P = torch.from_numpy(pts).to(dev)
     B = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
@@ -226,7 +229,7 @@ def run_ours(args, cfg):
     launches = 0.0
     keys = ("schur_ms", "schur_flops", "schur_bytes", "schur_launches", "pivot_ms", "pivot_flops", "pivot_bytes",
             "tri_ms", "tri_flops", "tri_bytes", "pqr_ms", "pqr_bytes", "redir_ms", "redir_flops", "redir_bytes",
-            "factor_flops", "max_rank", "compressions", "device_bytes", "host_syncs",
+            "factor_flops", "max_rank", "compressions", "device_bytes", "host_syncs", "dist_bytes", "dist_exchanges",
             "mult_ms", "mult_flops", "proj_ms", "proj_flops", "fresh_ms", "fresh_flops", "orth_ms")
     for _ in range(args.steps):
         flush.fill_(1.0)
@@ -248,7 +251,7 @@ def run_ours(args, cfg):
     step_ms = (tb + tf + ts) / K
     fs_ms = (tf + ts) / K
     fs_ms, step_ms = D.max_over_ranks([fs_ms, step_ms], dev)
-    value = D.aggregate_throughput(cfg.n, world, fs_ms / 1e3)
+    value = D.strong_throughput(cfg.n, fs_ms / 1e3)
 
     # correctness guard on the last device result: direct-sum residual on the GPU (row a9,
     # aifmm_residual) over the 4096 sampled rows
@@ -273,7 +276,7 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         if it > 0:
             e2e_t.append(time.perf_counter() - t0)
-    e2e_value = D.aggregate_throughput(cfg.n, world, D.max_over_ranks([float(np.mean(e2e_t))], dev)[0])
+    e2e_value = D.strong_throughput(cfg.n, D.max_over_ranks([float(np.mean(e2e_t))], dev)[0])
 
     if rank != 0:
         if world > 1:
@@ -334,8 +337,9 @@ def run_ours(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": _config_dict(cfg, parallelism="1 GPU" if world == 1 else f"{world} independent replicas (one per GPU)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(cfg, parallelism="1 GPU" if world == 1 else
+                               f"{world} GPUs: subtree split, owner computes, NCCL broadcast exchanges per phase",
                                l2="flushed (256 MB write) between steps; working set > L2"),
         "phase_ms": {"build": tb / K, "factor": tf / K, "solve": ts / K},
         "factor_phase_device_ms": phase_ms,
@@ -343,6 +347,7 @@ def run_ours(args, cfg):
         "factor_tflop_per_step": acc["factor_flops"] / K / 1e12,
         "max_rank": acc["max_rank"] / K, "compressions_per_step": acc["compressions"] / K,
         "device_gb": acc["device_bytes"] / K / 1e9, "host_syncs_per_step": acc["host_syncs"] / K,
+        "dist_exchange_gb_per_step": acc["dist_bytes"] / K / 1e9, "dist_exchanges_per_step": acc["dist_exchanges"] / K,
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": [round(t * 1e3, 2) for t in e2e_t],
                 "h2d_bytes_per_step": int(pts.nbytes + b.nbytes),
                 "d2h_bytes_per_step": int(b.nbytes), "includes": "H2D points, build, factor, H2D B, solve, D2H X; warm-up run excluded"},

@@ -48,7 +48,10 @@ class Comm {
  public:
   int rank = 0, world = 1, lp = -1;
   int kind = 0;   // 0 off, 1 NCCL, 2 in-process
-  bool on() const { return kind != 0 && world > 1; }
+  // force1 (AIFMM_DIST_FORCE=1, test hook): a world of one still runs the distributed code path
+  // (ownership, filtered batches, NCCL calls on a one-rank communicator)
+  bool force1 = false;
+  bool on() const { return kind != 0 && (world > 1 || force1); }
 
   ~Comm() { finalize(); }
 
@@ -59,6 +62,7 @@ class Comm {
     std::memcpy(&id, uid, sizeof(id));
     AIFMM_CUDA(cudaStreamSynchronize(s));
     nccl_check(p_init(&comm_, w, id, r), "ncclCommInitRank");
+    force1 = getenv("AIFMM_DIST_FORCE") != nullptr;
     rank = r;
     world = w;
     kind = 1;
@@ -83,6 +87,7 @@ class Comm {
     kind = 0;
     world = 1;
     rank = 0;
+    force1 = false;
   }
   static void unique_id(void* out) {
     load_nccl();
