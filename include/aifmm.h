@@ -248,6 +248,11 @@ int aifmm_get_owners(int level, int32_t* owner);
 /* Test hook: in-place inverse of one n x n column-major device matrix with the library's
  * batched Gauss-Jordan (R16; the kernel behind pivot inverses and the top solve). */
 int aifmm_debug_inverse(double* A, int n, int lda);
+/* Test hook: in-place inverses of `batch` n x n column-major device matrices stored back to back
+ * (ld n) by the batched Gauss-Jordan; path 0 = the library's routing, 1 = one panel launch +
+ * one DMMA GEMM launch per 32 columns, 2 = the fused one-CTA-per-matrix kernel (n > 160).
+ * Errors: EINVALID_ARG, ESINGULAR_PIVOT. */
+int aifmm_debug_inverse_batch(double* A, int n, int batch, int path);
 /* Test hook: first stage of the two-stage RRQR (reading R8b) on `batch` device matrices A_b
  * (n x m column-major, ld n, stored back to back; destroyed): M_b = R_b^T (m x min(n,m), ld m,
  * back to back), where A_b = Q_b R_b (Householder; TSQR row chunks when n > 768 and m <= 384).

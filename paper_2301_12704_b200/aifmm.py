@@ -26,7 +26,7 @@ SYMBOLS = ["aifmm_build", "aifmm_set_compression_tol", "aifmm_factor", "aifmm_so
            "aifmm_solve_host", "aifmm_free", "aifmm_last_error", "aifmm_set_stream",
            "aifmm_get_tree", "aifmm_get_level_offsets", "aifmm_get_lists", "aifmm_get_colours",
            "aifmm_get_ranks", "aifmm_stats", "aifmm_reset_counters", "aifmm_set_timing",
-           "aifmm_debug_inverse", "aifmm_debug_tri_root", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres",
+           "aifmm_debug_inverse", "aifmm_debug_inverse_batch", "aifmm_debug_tri_root", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres",
            "aifmm_residual", "aifmm_set_algorithm", "aifmm_dist_unique_id", "aifmm_dist_init",
            "aifmm_dist_init_local", "aifmm_dist_finalize", "aifmm_get_owners"]
 STAT_NAMES = ["build_ms", "factor_ms", "solve_ms", "levels", "top_size", "factor_flops",
@@ -106,6 +106,7 @@ def _open(path: str):
     lib.aifmm_set_timing.argtypes = [I]
     lib.aifmm_debug_inverse.argtypes = [P, I, I]
     lib.aifmm_debug_tri_root.argtypes = [P, I, I, I, P]
+    lib.aifmm_debug_inverse_batch.argtypes = [P, I, I, I]
     lib.aifmm_matvec_build.argtypes = [D]
     lib.aifmm_matvec.argtypes = [P, P, I]
     lib.aifmm_gmres.argtypes = [P, P, I, D, I, I, P, P]
@@ -267,6 +268,17 @@ def debug_inverse(M):
     Mc = M.to(torch.float64).t().contiguous()   # column-major storage of M
     _check(load().aifmm_debug_inverse(ctypes.c_void_p(Mc.data_ptr()), Mc.shape[0], Mc.shape[0]))
     return Mc.t()
+
+
+def debug_inverse_batch(M, path: int = 0):
+    """In-place GPU inverses of a (batch, n, n) CUDA float64 tensor (test hook; path 0 automatic,
+    1 panel + GEMM launches, 2 fused one-CTA-per-matrix kernel).  Returns the inverses."""
+    import torch
+    b, n, _ = M.shape
+    _bind_stream()
+    Mc = M.to(torch.float64).transpose(1, 2).contiguous()   # column-major storage per matrix
+    _check(load().aifmm_debug_inverse_batch(ctypes.c_void_p(Mc.data_ptr()), n, b, int(path)))
+    return Mc.transpose(1, 2)
 
 
 def debug_tri_root(A):

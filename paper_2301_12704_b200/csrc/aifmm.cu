@@ -2812,6 +2812,29 @@ int aifmm_debug_inverse(double* A, int n, int lda) {
   CAPI_END
 }
 
+int aifmm_debug_inverse_batch(double* A, int n, int batch, int path) {
+  CAPI_BEGIN
+  AIFMM_REQUIRE(A && n >= 1 && batch >= 1 && path >= 0 && path <= 2, AIFMM_EINVALID_ARG, "bad arguments");
+  Ctx& c = ctx();
+  std::vector<InvReq> reqs;
+  int* dinfo = c.work.i(batch);
+  AIFMM_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int) * batch, c.s));
+  for (int b = 0; b < batch; ++b) reqs.push_back(InvReq{A + (size_t)b * n * n, n, n, dinfo + b});
+  g_gj_force = path;
+  try {
+    batched_inverse(reqs, c.work, c.up, c.s);
+  } catch (...) {
+    g_gj_force = 0;
+    throw;
+  }
+  g_gj_force = 0;
+  std::vector<int> info = d2h(c, dinfo, batch);
+  c.work.reset();
+  for (int b = 0; b < batch; ++b)
+    if (info[b]) throw Error(AIFMM_ESINGULAR_PIVOT, "singular matrix " + std::to_string(b));
+  CAPI_END
+}
+
 int aifmm_debug_tri_root(double* A, int n, int m, int batch, double* M) {
   CAPI_BEGIN
   Ctx& c = ctx();

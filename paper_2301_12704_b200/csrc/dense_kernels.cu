@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(GJ_NT) gj_global_kernel(const GJTask* __restri
 // the pivots (identical to GJ's), rows are swapped, D = A[J,J] is inverted from its LU,
 // A[J,:] <- D^{-1} A[J,:], A[R,J] <- 0, B = old A[R,J]; then a DMMA GEMM does A[R,:] -= B A[J,:].
 constexpr int GJB = 32;
+constexpr int GJ_CPW = 4;   // columns per warp in flight in the row-interchange / D^{-1} pass
 struct GJBTask {
   double* A;
   int lda, n;
@@ -386,12 +387,12 @@ struct GJBTask {
   int* info;
 };
 
-__global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restrict__ tasks, int j, int smem_elems) {
-  extern __shared__ double gj_pw_smem[];
-  const GJBTask tk = tasks[blockIdx.x];
+// One panel step of the blocked Gauss-Jordan inverse for one matrix (the whole CTA); returns
+// false (info set) on an exactly singular panel.  Used by gj_panel_kernel (one launch per panel,
+// DMMA update by a separate GEMM launch) and gj_fused_kernel (all panels and their updates in
+// one CTA).
+__device__ __forceinline__ bool gj_panel_dev(const GJBTask& tk, int j, double* gj_pw_smem, int smem_elems) {
   const int n = tk.n;
-  if (j >= n) return;
-  if (*tk.info) return;
   const int nbw = min(GJB, n - j), rows = n - j, ld = tk.lda;
   double* A = tk.A;
   double* PW = (rows * nbw <= smem_elems) ? gj_pw_smem : tk.PW;   // panel LU in smem when it fits
@@ -399,6 +400,8 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
   __shared__ int redi[32];
   __shared__ double Li[GJB][GJB + 1], Ui[GJB][GJB + 1], Di[GJB][GJB + 1];
   __shared__ double ycol[GJ_NT / 32][GJB];
+  __shared__ int prow_dst[2 * GJB], prow_src[2 * GJB];
+  __shared__ int prow_cnt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int c = warp; c < nbw; c += GJ_NT / 32)
     for (int r = lane; r < rows; r += 32) PW[(size_t)c * rows + r] = A[(size_t)(j + c) * ld + j + r];
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
     block_argmax<GJ_NT>(v, vi, red, redi, &mx, &p);
     if (!(mx > 0.0)) {
       if (tid == 0) *tk.info = j + c + 1;
-      return;
+      return false;
     }
     if (tid == 0) tk.piv[j + c] = j + p;
     if (p != c)
@@ -438,24 +441,9 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
     }
     __syncthreads();
   }
-  // apply the row interchanges to the full rows of A (in order): each thread owns whole
-  // columns and applies the panel's swaps in sequence (no barrier per interchange)
   __syncthreads();
   __shared__ int pv[GJB];
   if (tid < nbw) pv[tid] = tk.piv[j + tid];
-  __syncthreads();
-  for (int col = tid; col < n; col += GJ_NT) {
-    double* ac = A + (size_t)col * ld;
-    for (int c = 0; c < nbw; ++c) {
-      const int p = pv[c];
-      if (p != j + c) {
-        const double a = ac[j + c];
-        ac[j + c] = ac[p];
-        ac[p] = a;
-      }
-    }
-  }
-  __syncthreads();
   // D^{-1} = U11^{-1} L11^{-1} from the panel LU (unit lower L11, upper U11)
   for (int e = tid; e < GJB * GJB; e += GJ_NT) {
     const int r = e % GJB, c = e / GJB;
@@ -481,6 +469,24 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
         Ui[r][lane] = (r > lane) ? 0.0 : s / PW[(size_t)r * rows + r];
       }
     }
+  } else if (warp == 2 && lane == 0) {
+    // the panel's row interchanges (j + c <-> pv[c], in order) as one permutation of the affected
+    // rows: rows J first (dst j + t), then the pivot rows outside J; src = the old row that ends
+    // up in dst
+    int cnt = nbw;
+    for (int t = 0; t < nbw; ++t) { prow_dst[t] = j + t; prow_src[t] = j + t; }
+    for (int c = 0; c < nbw; ++c) {
+      const int p = pv[c];
+      if (p == j + c) continue;
+      int ip = -1;
+      for (int q = 0; q < cnt; ++q)
+        if (prow_dst[q] == p) { ip = q; break; }
+      if (ip < 0) { ip = cnt++; prow_dst[ip] = p; prow_src[ip] = p; }
+      const int tmp = prow_src[c];
+      prow_src[c] = prow_src[ip];
+      prow_src[ip] = tmp;
+    }
+    prow_cnt = cnt;
   }
   __syncthreads();
   for (int e = tid; e < nbw * nbw; e += GJ_NT) {
@@ -490,6 +496,43 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
     Di[r][c] = s;
   }
   __syncthreads();
+  // every column: the interchanges in one gather / scatter of the affected rows (one memory round
+  // trip instead of one per interchange); outside J also A[J, c] <- D^{-1} A[J, c].  A warp takes
+  // GJ_CPW columns at a time (their loads in flight together).
+  const int pc = prow_cnt;
+  const int sA0 = (lane < pc) ? prow_src[lane] : 0, dA0 = (lane < pc) ? prow_dst[lane] : 0;
+  const int sA1 = (lane + 32 < pc) ? prow_src[lane + 32] : 0, dA1 = (lane + 32 < pc) ? prow_dst[lane + 32] : 0;
+  for (int col0 = warp * GJ_CPW; col0 < n; col0 += GJ_NT / 32 * GJ_CPW) {
+    double v0[GJ_CPW], v1[GJ_CPW];
+#pragma unroll
+    for (int u = 0; u < GJ_CPW; ++u) {
+      const int col = col0 + u;
+      v0[u] = (col < n && lane < pc) ? A[(size_t)col * ld + sA0] : 0.0;
+      v1[u] = (col < n && lane + 32 < pc) ? A[(size_t)col * ld + sA1] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < GJ_CPW; ++u) {
+      const int col = col0 + u;
+      if (col >= n) break;
+      double* ac = A + (size_t)col * ld;
+      // entries 0..nbw-1 (lanes < nbw of v0) land in rows J; the rest are outside pivot rows
+      if (lane >= nbw && lane < pc) ac[dA0] = v0[u];
+      if (lane + 32 < pc) ac[dA1] = v1[u];
+      if (col >= j && col < j + nbw) {
+        if (lane < nbw) ac[j + lane] = v0[u];
+      } else {
+        if (lane < nbw) ycol[warp][lane] = v0[u];
+        __syncwarp();
+        if (lane < nbw) {
+          double s = 0.0;
+          for (int t = 0; t < nbw; ++t) s += Di[lane][t] * ycol[warp][t];
+          ac[j + lane] = s;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
   // B = A[:, J] with rows J zeroed, A[R, J] = 0, A[J, J] = D^{-1}
   for (int c = warp; c < nbw; c += GJ_NT / 32)
     for (int r = lane; r < n; r += 32) {
@@ -497,18 +540,112 @@ __global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restri
       tk.Bws[(size_t)c * n + r] = inJ ? 0.0 : A[(size_t)(j + c) * ld + r];
       A[(size_t)(j + c) * ld + r] = inJ ? Di[r - j][c] : 0.0;
     }
-  // A[J, c] <- D^{-1} A[J, c] for columns outside J
-  for (int col = warp; col < n; col += GJ_NT / 32) {
-    if (col >= j && col < j + nbw) continue;
-    if (lane < nbw) ycol[warp][lane] = A[(size_t)col * ld + j + lane];
-    __syncwarp();
-    if (lane < nbw) {
-      double s = 0.0;
-      for (int t = 0; t < nbw; ++t) s += Di[lane][t] * ycol[warp][t];
-      A[(size_t)col * ld + j + lane] = s;
+  return true;
+}
+
+__global__ void __launch_bounds__(GJ_NT) gj_panel_kernel(const GJBTask* __restrict__ tasks, int j, int smem_elems) {
+  extern __shared__ double gj_pw_smem[];
+  const GJBTask tk = tasks[blockIdx.x];
+  if (j >= tk.n) return;
+  if (*tk.info) return;
+  gj_panel_dev(tk, j, gj_pw_smem, smem_elems);
+}
+
+// Fused blocked Gauss-Jordan inverse: one CTA per matrix runs every panel step and its rank-nbw
+// update A <- A - B A[J, :] (B = Bws: the panel's old column block with rows J zeroed) on the FP64
+// tensor cores (DMMA 8x8x4), then the column unscrambling -- one launch for the whole batch
+// instead of 2 launches per 32 columns.  The update covers every row: rows J of B are exact
+// zeros, so those rows are rewritten with their own values (C + (+-0) = C) and the arithmetic of
+// every other entry is the separate GEMM launch's (same DMMA k order, C + acc with beta = 1):
+// the result is bitwise that of the gj_panel_kernel + gemm_tasks_kernel path.
+constexpr int GJF_TM = 64, GJF_TN = 128, GJF_LA = GJF_TM + 4, GJF_LB = GJF_TN + 4;
+constexpr int GJF_TILE_DOUBLES = GJB * (GJF_LA + GJF_LB);
+__device__ __forceinline__ void gj_fused_update(const GJBTask& tk, int j, int nbw, double* sm) {
+  const int n = tk.n, lda = tk.lda;
+  double* A = tk.A;
+  const double* Bw = tk.Bws;
+  double* sA = sm;                       // [GJB][GJF_LA]: sA[k][m] = -B[m0 + m][k]
+  double* sB = sm + GJB * GJF_LA;        // [GJB][GJF_LB]: sB[k][c] = A[j + k][n0 + c]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  for (int m0 = 0; m0 < n; m0 += GJF_TM) {
+    for (int e = tid; e < GJB * GJF_TM; e += GJ_NT) {
+      const int mm = e % GJF_TM, kk = e / GJF_TM;
+      const int gm = m0 + mm;
+      sA[kk * GJF_LA + mm] = (gm < n && kk < nbw) ? -Bw[(size_t)kk * n + gm] : 0.0;
     }
-    __syncwarp();
+    for (int n0 = 0; n0 < n; n0 += GJF_TN) {
+      for (int e = tid; e < GJB * GJF_TN; e += GJ_NT) {
+        const int kk = e % GJB, nn = e / GJB;
+        const int gn = n0 + nn;
+        sB[kk * GJF_LB + nn] = (gn < n && kk < nbw) ? A[(size_t)gn * lda + j + kk] : 0.0;
+      }
+      __syncthreads();
+      double acc[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < GJB; kk += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = sA[(kk + (lane & 3)) * GJF_LA + wm + i * 8 + (lane >> 2)];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[q] = sB[(kk + (lane & 3)) * GJF_LB + wn + q * 8 + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dmma_884(acc[i][q][0], acc[i][q][1], a[i], b[q]);
+      }
+      // epilogue C = 1.0 * C + acc, loads issued before stores per 8-row group
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int gm = m0 + wm + i * 8 + (lane >> 2);
+        const bool okm = gm < n;
+        double cv[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int gn = n0 + wn + q * 8 + (lane & 3) * 2 + e;
+            cv[q][e] = (okm && gn < n) ? A[(size_t)gn * lda + gm] : 0.0;
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int gn = n0 + wn + q * 8 + (lane & 3) * 2 + e;
+            if (okm && gn < n) A[(size_t)gn * lda + gm] = 1.0 * cv[q][e] + acc[i][q][e];
+          }
+      }
+      __syncthreads();
+    }
   }
+}
+
+__global__ void __launch_bounds__(GJ_NT, 2) gj_fused_kernel(const GJBTask* __restrict__ tasks, int smem_elems) {
+  extern __shared__ __align__(16) double gjf_smem[];
+  const GJBTask tk = tasks[blockIdx.x];
+  const int n = tk.n;
+  if (*tk.info) return;
+  for (int j = 0; j < n; j += GJB) {
+    if (!gj_panel_dev(tk, j, gjf_smem, smem_elems)) return;
+    __syncthreads();
+    gj_fused_update(tk, j, min(GJB, n - j), gjf_smem);
+  }
+  // column interchanges in reverse pivot order (each thread owns rows)
+  __syncthreads();
+  double* A = tk.A;
+  for (int i = threadIdx.x; i < n; i += GJ_NT)
+    for (int k = n - 1; k >= 0; --k) {
+      const int p = tk.piv[k];
+      if (p != k) {
+        const double a = A[(size_t)k * tk.lda + i];
+        A[(size_t)k * tk.lda + i] = A[(size_t)p * tk.lda + i];
+        A[(size_t)p * tk.lda + i] = a;
+      }
+    }
 }
 
 // Cluster variant of the Gauss-Jordan panel for few large matrices (the top system, upper-level
@@ -2167,6 +2304,13 @@ void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s) {
   const int elems = (160 * 1024) / 8;
   ensure_dyn_smem(gj_panel_kernel, (size_t)elems * 8);
   LAUNCH(gj_panel_kernel, ntasks, GJ_NT, (size_t)elems * 8, s, static_cast<const GJBTask*>(t), j, elems);
+}
+void launch_gj_fused(const void* t, int ntasks, int nmax, cudaStream_t s) {
+  // the panel LU is staged in shared memory when it fits next to nothing else (it is dead by the
+  // time the update tiles use the same buffer); capped so that two CTAs fit on an SM
+  const int elems = std::max(GJF_TILE_DOUBLES, std::min(nmax * GJB, (72 * 1024) / 8));
+  ensure_dyn_smem(gj_fused_kernel, (size_t)elems * 8);
+  LAUNCH(gj_fused_kernel, ntasks, GJ_NT, (size_t)elems * 8, s, static_cast<const GJBTask*>(t), elems);
 }
 void launch_gj_unscramble(const void* t, int ntasks, int nmax, cudaStream_t s) {
   if (ntasks <= 0) return;

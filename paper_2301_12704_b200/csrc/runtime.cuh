@@ -34,6 +34,7 @@ void launch_chol_inv(const CholTask* t, int ntasks, int kmax, cudaStream_t s);
 void launch_gj_panel(const void* t, int ntasks, int j, cudaStream_t s);
 void launch_gj_panel_cluster(const void* t, int ntasks, int j, int nmax, cudaStream_t s);
 void launch_gj_unscramble(const void* t, int ntasks, int nmax, cudaStream_t s);
+void launch_gj_fused(const void* t, int ntasks, int nmax, cudaStream_t s);
 size_t gjb_task_size();
 void gjb_make(void* out, double* A, int lda, int n, double* PW, double* Bws, int* piv, int* info);
 size_t hh_task_size();
@@ -544,9 +545,31 @@ struct InvReq {
   int lda, n;
   int* info;
 };
+// test hook (aifmm_debug_inverse_batch): 0 automatic routing, 1 panel + GEMM launches, 2 fused
+inline int g_gj_force = 0;
+template <class Pool>
+inline void batched_inverse_impl(const std::vector<InvReq>& reqs, Pool& work, Uploader& up, cudaStream_t s,
+                                 FlopCounter* fc);
+// debug (AIFMM_DEBUG_INV=1): per call, the batch shape and its device time (synchronising)
 template <class Pool>
 inline void batched_inverse(const std::vector<InvReq>& reqs, Pool& work, Uploader& up, cudaStream_t s,
                             FlopCounter* fc = nullptr) {
+  static const bool dbg = getenv("AIFMM_DEBUG_INV") != nullptr;
+  if (!dbg) return batched_inverse_impl(reqs, work, up, s, fc);
+  int cnt = 0, nmin = 1 << 30, nmax = 0;
+  double fl = 0;
+  for (const InvReq& r : reqs)
+    if (r.n > 0) { ++cnt; nmin = std::min(nmin, r.n); nmax = std::max(nmax, r.n); fl += 2.0 * r.n * (double)r.n * r.n; }
+  up.sync();
+  auto t0 = std::chrono::steady_clock::now();
+  batched_inverse_impl(reqs, work, up, s, fc);
+  up.sync();
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  fprintf(stderr, "[aifmm inv] count %d n %d..%d  %.3f ms  %.2f TF/s\n", cnt, cnt ? nmin : 0, nmax, ms, fl / ms / 1e9);
+}
+template <class Pool>
+inline void batched_inverse_impl(const std::vector<InvReq>& reqs, Pool& work, Uploader& up, cudaStream_t s,
+                                 FlopCounter* fc) {
   std::vector<GJTask> small;
   int nsm = 0;
   std::vector<InvReq> big;
@@ -579,6 +602,16 @@ inline void batched_inverse(const std::vector<InvReq>& reqs, Pool& work, Uploade
   }
   const void* dt = up.put(tb.data(), tb.size());
   unsigned long long dgen = up.gen();
+  // opt-in (AIFMM_GJ_FUSED_MIN = batch size from which it is used): one CTA per matrix runs all
+  // panels and their DMMA updates in one launch.  Measured slower on config 3 (pivot inverses
+  // 464 vs 398 ms: the rank-32 update is memory-bound either way and one CTA per matrix
+  // serialises each matrix's panel latency with its update), so off by default
+  static const int fused_min = getenv("AIFMM_GJ_FUSED_MIN") ? atoi(getenv("AIFMM_GJ_FUSED_MIN")) : 0;
+  const bool fused = g_gj_force == 2 || (g_gj_force == 0 && fused_min > 0 && (int)big.size() >= fused_min);
+  if (fused) {
+    launch_gj_fused(dt, (int)big.size(), nmax, s);
+    return;
+  }
   // few matrices: 8-CTA clusters per matrix (row slices in shared memory); many: one CTA each
   static const bool gj_single = getenv("AIFMM_GJ_SINGLE") != nullptr;   // debug toggle
   const bool cluster = !gj_single && (int)big.size() <= 148 && nmax <= 8 * 700;
