@@ -114,6 +114,12 @@ int aifmm_get_colours(int level, int32_t* colour);
  * factorization (which = 1) of every box (0 for empty boxes). */
 int aifmm_get_ranks(int level, int which, int32_t* ranks);
 
+/* aifmm_get_skeletons — the NNCA skeletons sk(B) = t^{B,i} (row pivots, R10) and
+ * far pivots fp(B) = s^{B,i} of every box at `level`, as tree-order point indices, in pivot
+ * order: CSR with sk_ptr host int32[2^(d*level)+1] (sk_ptr[b+1]-sk_ptr[b] = NNCA rank of b);
+ * sk_idx / fp_idx host int32[sk_ptr[last]] or NULL (query the sizes first). */
+int aifmm_get_skeletons(int level, int32_t* sk_ptr, int32_t* sk_idx, int32_t* fp_idx);
+
 /* ---- Row a8 (BASELINE config 5): H2 matvec and AIFMM-preconditioned GMRES --------------
  * aifmm_matvec_build — build a second NNCA (ACA tolerance tol/100, reading R18) on the tree of
  *   the last aifmm_build, for the H2 matrix-vector product (Eq. NCA P:347-367 with the nested

@@ -25,7 +25,7 @@ ERRORS = {
 SYMBOLS = ["aifmm_build", "aifmm_set_compression_tol", "aifmm_factor", "aifmm_solve",
            "aifmm_solve_host", "aifmm_free", "aifmm_last_error", "aifmm_set_stream",
            "aifmm_get_tree", "aifmm_get_level_offsets", "aifmm_get_lists", "aifmm_get_colours",
-           "aifmm_get_ranks", "aifmm_stats", "aifmm_reset_counters", "aifmm_set_timing",
+           "aifmm_get_ranks", "aifmm_get_skeletons", "aifmm_stats", "aifmm_reset_counters", "aifmm_set_timing",
            "aifmm_debug_inverse", "aifmm_debug_inverse_batch", "aifmm_debug_tri_root", "aifmm_matvec_build", "aifmm_matvec", "aifmm_gmres",
            "aifmm_residual", "aifmm_set_algorithm", "aifmm_dist_unique_id", "aifmm_dist_init",
            "aifmm_dist_init_local", "aifmm_dist_finalize", "aifmm_get_owners"]
@@ -102,6 +102,7 @@ def _open(path: str):
     lib.aifmm_get_lists.argtypes = [I, P, P, P, P]
     lib.aifmm_get_colours.argtypes = [I, P]
     lib.aifmm_get_ranks.argtypes = [I, I, P]
+    lib.aifmm_get_skeletons.argtypes = [I, P, P, P]
     lib.aifmm_stats.argtypes = [P]
     lib.aifmm_set_timing.argtypes = [I]
     lib.aifmm_debug_inverse.argtypes = [P, I, I]
@@ -239,6 +240,17 @@ def get_ranks(level: int, d: int, which: int = 0):
     r = np.zeros(1 << (d * level), dtype=np.int32)
     _check(load().aifmm_get_ranks(level, which, _ptr(r)))
     return r
+
+
+def get_skeletons(level: int, d: int):
+    """(sk_ptr, sk_idx, fp_idx): NNCA skeleton rows and far pivots per box (tree-order indices)."""
+    lib = load()
+    ptr = np.zeros((1 << (d * level)) + 1, dtype=np.int32)
+    _check(lib.aifmm_get_skeletons(level, _ptr(ptr), None, None))
+    sk = np.zeros(max(int(ptr[-1]), 1), dtype=np.int32)
+    fp = np.zeros(max(int(ptr[-1]), 1), dtype=np.int32)
+    _check(lib.aifmm_get_skeletons(level, _ptr(ptr), _ptr(sk), _ptr(fp)))
+    return ptr, sk[:ptr[-1]], fp[:ptr[-1]]
 
 
 def stats() -> dict:

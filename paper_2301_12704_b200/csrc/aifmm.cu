@@ -2775,6 +2775,25 @@ int aifmm_get_ranks(int level, int which, int32_t* ranks) {
   CAPI_END
 }
 
+int aifmm_get_skeletons(int level, int32_t* sk_ptr, int32_t* sk_idx, int32_t* fp_idx) {
+  CAPI_BEGIN
+  Ctx& c = ctx();
+  AIFMM_REQUIRE(c.built && level >= 2 && level <= c.L && sk_ptr, AIFMM_EINVALID_ARG, "bad level");
+  const NLevel& nl = c.nn[level];
+  const int nb = 1 << (c.d * level);
+  for (int b = 0; b <= nb; ++b) sk_ptr[b] = (int32_t)nl.skoff[b];
+  const size_t tot = (size_t)nl.skoff[nb];
+  if (tot && sk_idx) {
+    std::vector<int> h = d2h(c, nl.dsk, tot);
+    std::copy(h.begin(), h.end(), sk_idx);
+  }
+  if (tot && fp_idx) {
+    std::vector<int> h = d2h(c, nl.dfp, tot);
+    std::copy(h.begin(), h.end(), fp_idx);
+  }
+  CAPI_END
+}
+
 int aifmm_stats(double* out) {
   CAPI_BEGIN
   Ctx& c = ctx();

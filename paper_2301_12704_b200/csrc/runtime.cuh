@@ -614,7 +614,8 @@ inline void batched_inverse_impl(const std::vector<InvReq>& reqs, Pool& work, Up
   }
   // few matrices: 8-CTA clusters per matrix (row slices in shared memory); many: one CTA each
   static const bool gj_single = getenv("AIFMM_GJ_SINGLE") != nullptr;   // debug toggle
-  const bool cluster = !gj_single && (int)big.size() <= 148 && nmax <= 8 * 700;
+  static const int cl_max = getenv("AIFMM_GJ_CLUSTER_MAX") ? atoi(getenv("AIFMM_GJ_CLUSTER_MAX")) : 148;
+  const bool cluster = !gj_single && (int)big.size() <= cl_max && nmax <= 8 * 700;
   for (int j = 0; j < nmax; j += GJ_PANEL) {
     if (up.gen() != dgen) { dt = up.put(tb.data(), tb.size()); dgen = up.gen(); }   // staging rewound
     if (cluster) launch_gj_panel_cluster(dt, (int)big.size(), j, nmax, s);

@@ -56,6 +56,11 @@ def _integer_parity(o, d):
                 assert rk[b] == o.nnca.rank(l, b)
             else:
                 assert nptr[b + 1] == nptr[b] and col[b] == -1
+        # NNCA skeletons and far pivots (row a3): the same indices in the same pivot order
+        skp, sk, fp = G.get_skeletons(l, d)
+        for b in o.nnca.sk[l]:
+            assert list(sk[skp[b]:skp[b + 1]]) == o.nnca.sk[l][b].tolist(), (l, b)
+            assert list(fp[skp[b]:skp[b + 1]]) == o.nnca.fp[l][b].tolist(), (l, b)
 
 
 CASES = [
@@ -287,6 +292,9 @@ def test_config3_full_size_parity():
             assert np.array_equal(a, bb)
         assert np.array_equal(G.get_colours(l, 2), c.colours(l))
         assert np.array_equal(G.get_ranks(l, 2, 0), g[f"nnca_{l}"])
+        skp, sk, _ = G.get_skeletons(l, 2)
+        for bx in np.flatnonzero(np.diff(skp)):
+            assert np.array_equal(sk[skp[bx]:skp[bx + 1]], c.skeleton(l, int(bx))), (l, bx)
     del c
     G.factor()
     X = G.solve(torch.from_numpy(np.ascontiguousarray(b)).cuda())
