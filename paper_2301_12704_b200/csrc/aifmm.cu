@@ -536,7 +536,7 @@ static void build_nnca(Ctx& c, std::vector<NLevel>& nnv, double eps, DevPool& po
         size_t need = (size_t)kmaxv[b] * (nl.nR[b] + nF[b]) * 8 + nl.nR[b] + nF[b] + 1024;
         if (!tasks.empty() && ws + need > budget) break;
         ws += need;
-        if (kmaxv[b] > 0) {
+        if (kmaxv[b] > 0 && c.mine(l, b)) {   // §8(e): a rank runs the ACA of its own boxes
           AcaTask t{};
           t.R = nl.dR + nl.Roff[b];
           t.frange = dfr + 2 * froff[b];
@@ -571,6 +571,18 @@ static void build_nnca(Ctx& c, std::vector<NLevel>& nnv, double eps, DevPool& po
     }
     c.work.reset();
     nl.k = d2h(c, drank, nb);
+    if (c.dist_level(l)) {   // §8(e): the owners' ranks and pivots (non-owners hold zeros)
+      c.comm.allreduce_int(nl.k.data(), nb, c.s);
+      for (int w = 0; w < 2; ++w) {
+        int* dp = w ? dcp : drp;
+        std::vector<int> h = d2h(c, dp, (size_t)std::max<long long>(pivtot, 1));
+        for (int b = 0; b < nb; ++b)
+          for (long long q = pivoff[b] + (c.mine(l, b) ? nl.k[b] : 0); q < pivoff[b + 1]; ++q) h[q] = 0;
+        c.comm.allreduce_int(h.data(), (int)h.size(), c.s);
+        AIFMM_CUDA(cudaMemcpyAsync(dp, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, c.s));
+        c.up.sync();
+      }
+    }
     // skeleton / far-pivot arrays compacted by box
     nl.skoff.assign(nb + 1, 0);
     for (int b = 0; b < nb; ++b) nl.skoff[b + 1] = nl.skoff[b] + nl.k[b];
@@ -600,7 +612,7 @@ static void build_nnca(Ctx& c, std::vector<NLevel>& nnv, double eps, DevPool& po
     AIFMM_CUDA(cudaMemsetAsync(c.dflag, 0, sizeof(int), c.s));
     for (int b : boxes) {
       const int k = nl.k[b], nr = nl.nR[b];
-      if (!k) continue;
+      if (!k || !c.mine(l, b)) continue;
       double* aug = c.work.d((size_t)k * (k + nr));
       kt.push_back(KEvalTask{aug, k, k, k, nl.dfp + nl.skoff[b], nl.dsk + nl.skoff[b], 0, 0});
       kt.push_back(KEvalTask{aug + (size_t)k * k, k, k, nr, nl.dfp + nl.skoff[b], nl.dR + nl.Roff[b], 0, 0});
@@ -619,6 +631,12 @@ static void build_nnca(Ctx& c, std::vector<NLevel>& nnv, double eps, DevPool& po
       if (!gs.empty()) launch_gj(c.up.put(gs), (int)gs.size(), (int)smem_s, 0, c.s);
       if (!gg.empty()) launch_gj(c.up.put(gg), (int)gg.size(), -nmax_g, 0, c.s);
       cb.run(c.up, c.s);
+    }
+    if (c.dist_level(l)) {   // §8(e): the owners' operators U_B
+      std::vector<std::vector<Region>> reg(c.comm.world);
+      for (int b : boxes)
+        if (nl.k[b] && nl.nR[b]) reg[c.own(l, b)].push_back(Region{nl.dU + nl.Uoff[b], nl.nR[b], nl.nR[b], nl.k[b]});
+      c.comm.exchange(reg, c.up, c.s);
     }
     check_flag(c, AIFMM_ECOINCIDENT, "coincident points with a singular kernel");
     std::vector<int> info = d2h(c, dinfo, nb);
@@ -2562,6 +2580,7 @@ int aifmm_build(const double* points, int64_t n, int d, int kernel_id, const dou
   g_prof.begin(c.s);
   build_tree(c, points);
   g_prof.end("tree");
+  plan_ownership(c);   // §8(e): the build's NNCA is split by subtree as well
   g_prof.begin(c.s);
   build_nnca(c);
   g_prof.end("nnca");

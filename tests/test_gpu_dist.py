@@ -61,7 +61,8 @@ def _run_ranks(world, pts, b, kid, kp, leaf, tol, level_p=-1, algorithm=3):
                 d = pts.shape[1]
                 out[rank] = dict(x=x, stats=G.stats(),
                                  owners={l: G.get_owners(l, d) for l in range(2, L + 1)},
-                                 ranks={l: G.get_ranks(l, d, 1) for l in range(2, L + 1)})
+                                 ranks={l: G.get_ranks(l, d, 1) for l in range(2, L + 1)},
+                                 sk={l: G.get_skeletons(l, d) for l in range(2, L + 1)})
                 G.dist_finalize()
                 G.set_algorithm(3)
                 G.free()
@@ -99,6 +100,8 @@ def test_distributed_factorization_in_process(case):
         for l in out[0]["ranks"]:
             assert np.array_equal(out[r]["ranks"][l], out[0]["ranks"][l])
             assert np.array_equal(out[r]["owners"][l], out[0]["owners"][l])
+            for a, bb in zip(out[r]["sk"][l], out[0]["sk"][l]):   # the split NNCA build
+                assert np.array_equal(a, bb)
     # the work was split: some level below l_p is owned, every rank owns boxes there
     split = [l for l, o in out[0]["owners"].items() if (o >= 0).any()]
     assert split, "no distributed level"
@@ -107,8 +110,11 @@ def test_distributed_factorization_in_process(case):
     for r in range(world):
         st = out[r]["stats"]
         assert st["dist_exchanges"] > 0 and st["dist_bytes"] > 0
-    # north_star bars against the oracle
+    # north_star bars against the oracle (NNCA skeletons bit-exact although the build was split)
     o = Oracle(pts, kid, kp, leaf, tol).factor()
+    for l, (skp, sk, fp) in out[0]["sk"].items():
+        for bx in o.nnca.sk[l]:
+            assert list(sk[skp[bx]:skp[bx + 1]]) == o.nnca.sk[l][bx].tolist()
     xo = o.solve(b)
     rel = np.linalg.norm(x0 - xo) / np.linalg.norm(xo)
     assert rel <= 10 * tol, rel
