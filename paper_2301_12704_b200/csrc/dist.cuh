@@ -74,6 +74,7 @@ class Comm {
     rank = r;
     world = w;
     kind = 2;
+    force1 = getenv("AIFMM_DIST_FORCE") != nullptr;
     my_sense_ = sh_->sense.load();   // every rank joins while no barrier is in flight
   }
   void finalize() {
