@@ -214,16 +214,18 @@ int aifmm_set_timing(int on);
 
 /* ---- the factorization split across ranks (one process per GPU) ------------
  * The paper's per-level loop (Alg. 3) runs colour by colour; the boxes of one
- * colour are independent (Remark P:402-404), so their work is split by subtree: the boxes of
- * the coarse level l_p are cut into `world` contiguous Morton ranges of about equal point
- * count, and a box below l_p belongs to the rank owning its level-l_p ancestor.
+ * colour are independent (Remark P:402-404), so their work is split by subtree: the points (in
+ * tree order) are cut into `world` contiguous ranges of equal size and a box belongs to the rank
+ * holding its median point -- contiguous Morton ranges of subtrees at the fine levels, one owner
+ * per box at the coarse ones.
  * Owner computes, state replicated: every rank builds the same tree / lists / NNCA and holds
  * every block; in each colour of a level below l_p a rank compresses (RRQR) only
  * its own boxes, inverts only its own pivots and forms their multipliers, and
  * performs only the Schur updates (Table 4) of target blocks whose row box it owns;
  * each of these three phases ends with an exchange that gives every rank the blocks the others
- * wrote (new basis columns with their ranks, G_i and W_i, updated targets).  Levels <= l_p,
- * the level set-up, orthonormalisation, redirection, new blocks, top and solve run
+ * wrote (new basis columns with their ranks, G_i and W_i, updated targets).  The NNCA build is
+ * split the same way (ACA and skeleton solves per owned box).  Levels <= level_p, the level
+ * set-up, orthonormalisation, redirection, new blocks, top and solve run
  * redundantly.  Every rank ends with the same factorization and solves locally.  The reading
  * R31 (null-space pivots) and the opt-in R30 are not used while distributed.
  *
@@ -231,8 +233,8 @@ int aifmm_set_timing(int on);
  *   the others, e.g. with torch.distributed.broadcast_object_list).  Errors: ENCCL.
  * aifmm_dist_init — join an NCCL communicator of `world` ranks as `rank` (one GPU per rank;
  *   the current CUDA device must be this rank's).  unique_id: host, 128 bytes from
- *   aifmm_dist_unique_id.  level_p: the partition level l_p (-1: automatic, the first level
- *   with at least 4 * world non-empty boxes, and below the leaf level).  Collective: every
+ *   aifmm_dist_unique_id.  level_p: levels <= level_p are computed redundantly by every rank
+ *   (-1: none, every level from 2 down is split; at most L - 1).  Collective: every
  *   rank calls it, then every rank calls build / factor with the SAME arguments.  A world of 1
  *   is the single-GPU path.  Errors: EINVALID_ARG, ENCCL.
  * aifmm_dist_init_local — the same over an in-process transport, for validation on one GPU:

@@ -560,9 +560,17 @@ static void build_nnca(Ctx& c, std::vector<NLevel>& nnv, double eps, DevPool& po
       // long far sets on few boxes (upper levels, 3D) go to the 8-CTA cluster kernel
       std::vector<AcaTask> small, big;
       int kbig = 1;
+      // AIFMM_ACA_CLUSTER_NF (experiment): far sets at least this long go to the cluster kernel at
+      // any box count (its 8 slices of a box's cross history stay L2-resident).  Measured on
+      // config 3: thresholds 8192 / 4096 / 2048 neutral, 1024 +45% build time; default off
+      static const int aca_cl_nf = getenv("AIFMM_ACA_CLUSTER_NF") ? atoi(getenv("AIFMM_ACA_CLUSTER_NF")) : (1 << 30);
       for (const AcaTask& t : tasks) {
-        if (t.nF >= 16384 || (boxes.size() < 512 && t.nF >= 1024)) { big.push_back(t); kbig = std::max(kbig, t.kmax); }
-        else small.push_back(t);
+        if (t.nF >= 16384 || t.nF >= aca_cl_nf || (boxes.size() < 512 && t.nF >= 1024)) {
+          big.push_back(t);
+          kbig = std::max(kbig, t.kmax);
+        } else {
+          small.push_back(t);
+        }
       }
       if (!small.empty()) launch_aca(c.up.put(small), (int)small.size(), c.pts, c.kp, eps, c.s);
       if (!big.empty()) launch_aca_cluster(c.up.put(big), (int)big.size(), kbig, c.pts, c.kp, eps, c.s);
@@ -1933,33 +1941,24 @@ static void deferred_checks(Ctx& c) {
   }
 }
 
-// §8(e): the boxes of level l_p are cut into world contiguous Morton ranges of about equal point
-// count (the rank of a box is that of its median point); a box below l_p belongs to the owner of
-// its level-l_p ancestor (Morton ids: b >> d (l - l_p)).  Levels <= l_p are redundant.
+// §8(e): the points (in tree order) are cut into world contiguous ranges of equal size; a box
+// belongs to the rank whose range holds its median point.  At the fine levels this is a split
+// into contiguous Morton ranges of subtrees; at the coarse levels, where a subtree split would
+// leave ranks idle, every box still has one owner.  Any ownership that all ranks agree on gives
+// the same factorisation (each phase exchanges every block it wrote); this one balances the
+// work level by level.  Levels <= l_p (default 1: none) are computed redundantly.
 static void plan_ownership(Ctx& c) {
   c.owner.assign(c.L + 1, {});
   c.lp = -1;
   if (!c.comm.on()) return;
   const int W = c.comm.world;
-  int lp = c.lp_user;
-  if (lp < 1) {
-    lp = c.L - 1;
-    for (int l = 2; l < c.L; ++l) {
-      int ne = 0;
-      for (int b = 0; b < (1 << (c.d * l)); ++b) ne += c.nonempty(l, b) ? 1 : 0;
-      if (ne >= 4 * W) { lp = l; break; }
-    }
-  }
-  lp = std::max(1, std::min(lp, c.L - 1));
-  c.lp = lp;
-  std::vector<int> own_p(1 << (c.d * lp), 0);
-  for (size_t b = 0; b < own_p.size(); ++b) {
-    const long long mid = c.off[lp][b] + (c.off[lp][b + 1] - c.off[lp][b]) / 2;
-    own_p[b] = (int)std::min<long long>(W - 1, mid * W / c.n);
-  }
-  for (int l = lp + 1; l <= c.L; ++l) {
+  c.lp = c.lp_user >= 1 ? std::min(c.lp_user, c.L - 1) : 1;
+  for (int l = c.lp + 1; l <= c.L; ++l) {
     c.owner[l].assign((size_t)1 << (c.d * l), 0);
-    for (size_t b = 0; b < c.owner[l].size(); ++b) c.owner[l][b] = own_p[b >> (c.d * (l - lp))];
+    for (size_t b = 0; b < c.owner[l].size(); ++b) {
+      const long long mid = c.off[l][b] + (c.off[l][b + 1] - c.off[l][b]) / 2;
+      c.owner[l][b] = (int)std::min<long long>(W - 1, mid * W / c.n);
+    }
   }
 }
 
