@@ -202,6 +202,10 @@ struct FLevel {
   BlkTable nearb;      // current version of near blocks (over N(p))
   BlkTable A, F;       // far M2L (cap kcap_p x kcap_q), far fill m_p x m_q (distance 2); over IL(p)
   std::set<std::pair<int, int>> pending;
+  // far fill-in slots live from their first Schur update to their compression (lazy_fill()):
+  // free slots by capacity (doubles), capacity of each F table slot
+  std::multimap<size_t, double*> ffree;
+  std::vector<size_t> fcap;
   std::vector<Rec> rec;
   std::vector<int> xoff;               // row offset of child c (level l+1 id) inside its parent's x
   std::vector<long long> xrow, zrow;   // solve layout
@@ -294,6 +298,14 @@ static std::string g_err;
 // (C_p = R_p^T), so the solve replays C_p through R_p^T and the blocks that would only serve
 // as C records live in the per-level scratch pool instead of the persistent record pool
 // (about half the near-block record memory).  AIFMM_FULL_RECORDS=1 keeps both (debug toggle).
+// Far fill-in slots (m_p x m_q, distance-2 pairs) are allocated when a Schur update first creates
+// the fill-in and recycled once it is compressed and redirected, instead of for every
+// distance-2 pair at the level start (AIFMM_EAGER_FILL=1 restores the latter).  Same arithmetic:
+// the creating update writes with beta = 0 where the eager slot held zeros.
+static bool lazy_fill() {
+  static const bool v = getenv("AIFMM_EAGER_FILL") == nullptr;
+  return v;
+}
 static bool half_records() {
   static const bool v = getenv("AIFMM_FULL_RECORDS") == nullptr;
   return v;
@@ -687,6 +699,8 @@ static void setup_level(Ctx& c, int l) {
   f.A.init(nb, c.icap, c.icnt[l].data(), c.iidx[l].data());
   f.F.init(nb, c.icap, c.icnt[l].data(), c.iidx[l].data());
   f.pending.clear();
+  f.ffree.clear();
+  f.fcap.assign((size_t)nb * c.icap, 0);
   const NLevel& nl = c.nn[l];
   FLevel* prev = (l < c.L) ? &c.fl[l + 1] : nullptr;
   if (prev) prev->xoff.assign(1 << (d * (l + 1)), 0);
@@ -733,7 +747,8 @@ static void setup_level(Ctx& c, int l) {
     for (int t = 0; t < ni; ++t) {
       int q = il[t];
       f.A.put_at(b, t) = Blk{carve((size_t)f.kcap[b] * f.kcap[q]), std::max(f.kcap[b], 1), f.k[b], f.k[q]};
-      if (c.cheb(l, b, q) == 2) f.F.put_at(b, t) = Blk{carve((size_t)f.m[b] * f.m[q]), std::max(f.m[b], 1), 0, 0};
+      if (c.cheb(l, b, q) == 2)
+        f.F.put_at(b, t) = Blk{lazy_fill() ? nullptr : carve((size_t)f.m[b] * f.m[q]), std::max(f.m[b], 1), 0, 0};
     }
   }
   for (auto& r : zr) AIFMM_CUDA(cudaMemsetAsync(r.first, 0, r.second, c.s));
@@ -1084,7 +1099,8 @@ static void compress_boxes(Ctx& c, FLevel& f, const std::vector<int>& aff, std::
     int o = 0;
     for (int q : part[b]) {
       const Blk& fb = f.F.at(f.key(b, q));   // row X_b, column of q: m x live_q -> transposed
-      cb.copy(fb.p, fb.ld, su[a].WT + o, nu, live(f, q), m, 1.0, /*trans=*/1);
+      if (fb.p) cb.copy(fb.p, fb.ld, su[a].WT + o, nu, live(f, q), m, 1.0, /*trans=*/1);
+      else cb.fill(su[a].WT + o, nu, live(f, q), m, 0.0);   // never created (a zero-size update)
       o += live(f, q);
     }
     nt.push_back(NormTask{su[a].WT, std::max(nu, 1), nu, m, dnorm + 2 * a});
@@ -1279,7 +1295,7 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
       if (!f.E[x] && !f.E[y]) {
         double* tp = c.work.d((size_t)f.m[x] * std::max(f.k[y], 1));
         g.task(tp, f.m[x], f.m[x], f.k[y], 0.0);
-        g.term(1.0, F.p, F.ld, 0, f.V[y], f.m[y], 0, f.m[y]);
+        if (F.p) g.term(1.0, F.p, F.ld, 0, f.V[y], f.m[y], 0, f.m[y]);
         p2p.push_back({{x, y}, tp});
       }
     }
@@ -1296,12 +1312,12 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
         g.term(1.0, f.U[x], f.m[x], 1, tp, f.m[x], 0, f.m[x]);
       } else if (f.E[x] && !f.E[y]) {
         g.task(A.p, A.ld, f.k[x], f.k[y], 1.0);
-        g.term(1.0, F.p, F.ld, 0, f.V[y], f.m[y], 0, f.m[y]);
+        if (F.p) g.term(1.0, F.p, F.ld, 0, f.V[y], f.m[y], 0, f.m[y]);
       } else {
         g.task(A.p, A.ld, f.k[x], f.k[y], 1.0);
-        g.term(1.0, f.U[x], f.m[x], 1, F.p, F.ld, 0, f.m[x]);
+        if (F.p) g.term(1.0, f.U[x], f.m[x], 1, F.p, F.ld, 0, f.m[x]);
       }
-      cb.fill(F.p, F.ld, live(f, x), live(f, y), 0.0);
+      if (!lazy_fill()) cb.fill(F.p, F.ld, live(f, x), live(f, y), 0.0);
     }
   g_prof.hlap("cmp.redirect");
   {
@@ -1314,6 +1330,19 @@ static void compress(Ctx& c, FLevel& f, const std::vector<std::pair<int, int>>& 
   }
   cb.run(c.up, c.s);
   for (auto& pr : S) f.pending.erase(pr);
+  if (lazy_fill()) {
+    // the compressed pairs' slots are free for later fill-ins: their next writer is planned
+    // after this point, so in stream order it follows these reads
+    for (auto& pr : S)
+      for (int dir = 0; dir < 2; ++dir) {
+        const int x = dir ? pr.second : pr.first, y = dir ? pr.first : pr.second;
+        const long long sl = f.F.slot(f.key(x, y));
+        Blk& F = f.F.v[sl];
+        if (!F.p) continue;
+        f.ffree.insert({f.fcap[sl], F.p});
+        F.p = nullptr;
+      }
+  }
   if (g_prof.on) g_prof.end("cmp.redirect");
 }
 
@@ -1417,13 +1446,33 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
       // R30: the (p, q) and (q, p) updates are transposes (symmetric kernel, V = U, R27); the
       // pair is planned once, at p < q (the contributing boxes are the same for both)
       if (p > q && !no_sym) continue;
+      bool fresh = false;   // a fill-in slot allocated by this update (written with beta = 0)
       auto target = [&](int x, int y) {
         Blk T;
         if (const Blk* it = f.nearb.get(f.key(x, y))) T = *it;
         else if (f.E[x] && f.E[y]) T = f.A.at(f.key(x, y));
         else {
-          T = f.F.at(f.key(x, y));
           AIFMM_REQUIRE(c.cheb(l, x, y) == 2, AIFMM_ESINGULAR_PIVOT, "fill-in outside N and IL");
+          const long long sl = f.F.slot(f.key(x, y));
+          AIFMM_REQUIRE(sl >= 0 && f.F.has[sl], AIFMM_ESINGULAR_PIVOT, "missing fill-in slot");
+          Blk& Fb = f.F.v[sl];
+          if (!Fb.p) {
+            const size_t need = std::max<size_t>((size_t)Fb.ld * f.m[y], 1);
+            auto it = f.ffree.lower_bound(need);
+            if (it != f.ffree.end() && it->first <= need + need / 4 + 1024) {
+              Fb.p = it->second;
+              f.fcap[sl] = it->first;
+              f.ffree.erase(it);
+            } else {
+              Fb.p = c.scr(l).d(need);
+              f.fcap[sl] = need;
+            }
+            fresh = true;
+            // R30 adds its mirrored temporaries onto the slots: those need zeros (stream order: the
+            // slot's previous readers were enqueued before this memset)
+            if (!no_sym) AIFMM_CUDA(cudaMemsetAsync(Fb.p, 0, sizeof(double) * need, c.s));
+          }
+          T = Fb;
         }
         return T;
       };
@@ -1432,7 +1481,7 @@ static void plan_schur(Ctx& c, FLevel& f, const std::vector<int>& cs, SchurPlan&
         P.mir.push_back({P.g.size(), T, target(q, p), M, N});
         P.g.task(nullptr, M, M, N, 0.0);   // temporary T_pq, allocated in eliminate_update
       } else {
-        P.g.task(T.p, T.ld, M, N, 1.0);
+        P.g.task(T.p, T.ld, M, N, fresh ? 0.0 : 1.0);
         P.towner.push_back(c.own(l, p));
         P.tblk.push_back(Blk{T.p, T.ld, M, N});
       }
@@ -1766,7 +1815,7 @@ static void dbg_symmetry(Ctx& c, FLevel& f, const char* where) {
         BlkTable& T = kind == 0 ? f.nearb : (kind == 1 ? f.A : f.F);
         const Blk* a = T.get(f.key(p, q));
         const Blk* b = T.get(f.key(q, p));
-        if (!a || !b) continue;
+        if (!a || !b || !a->p || !b->p) continue;
         if (kind == 2 && !f.pending.count({p, q})) continue;
         const int M = kind == 1 ? f.k[p] : live(f, p), N = kind == 1 ? f.k[q] : live(f, q);
         if (!M || !N) continue;
