@@ -4,7 +4,7 @@ tol-1e-10 H2 matvec, GMRES(30) to 1e-10.  For eps_A in {1e-3 (BASELINE), 1e-5 (t
 Exp. 5 value)}: factor time, the preconditioner's own relative residual
 ||A M^-1 b - b|| / ||b|| (direct sum on 4096 rows, aifmm_residual), GMRES iterations with the
 AIFMM preconditioner; and once per N the unpreconditioned and block-diagonal runs.
-Usage: python tools/gpu_cfg5_table.py N [maxit]   (one JSON line per run)"""
+Usage: python tools/gpu_cfg5_table.py N [maxit] [eps,eps,...]   (one JSON line per run)"""
 import sys, time, json
 sys.path.insert(0, '.')
 import numpy as np, torch
@@ -17,7 +17,8 @@ P = torch.from_numpy(pts).cuda()
 B = torch.from_numpy(np.ascontiguousarray(b[:, 0])).cuda()
 rows = W.residual_rows(n, cfg.seed)
 def t(): torch.cuda.synchronize(); return time.time()
-for eps in (1e-3, 1e-5):
+epss = [float(e) for e in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1e-3, 1e-5]
+for eps in epss:
     A.free()
     t0 = t(); A.build(P, cfg.kernel_id, cfg.kparams, cfg.leaf_size, eps); t1 = t()
     A.factor(); t2 = t()
