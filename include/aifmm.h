@@ -226,8 +226,9 @@ int aifmm_set_timing(int on);
  * wrote (new basis columns with their ranks, G_i and W_i, updated targets).  The NNCA build is
  * split the same way (ACA and skeleton solves per owned box).  Levels <= level_p, the level
  * set-up, orthonormalisation, redirection, new blocks, top and solve run
- * redundantly.  Every rank ends with the same factorization and solves locally.  The reading
- * R31 (null-space pivots) and the opt-in R30 are not used while distributed.
+ * redundantly.  Every rank ends with the same factorization and solves locally.  The pivots
+ * of the R31 (null-space) boxes are formed by every rank (their Schur operands are per-rank
+ * temporaries; their inverses are small); the opt-in R30 is not used while distributed.
  *
  * aifmm_dist_unique_id — host out[128]: a fresh NCCL unique id (call on one rank, send it to
  *   the others, e.g. with torch.distributed.broadcast_object_list).  Errors: ENCCL.

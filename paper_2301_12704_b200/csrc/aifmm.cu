@@ -1660,9 +1660,11 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     r.k = k;
     r.G = c.persist.d(std::max<size_t>((size_t)n * n, 1));
     if (!n) continue;
-    if (!c.mine(l, i, 2)) continue;   // §8(e): G_i arrives from owner(i)
-    // R31 is not used while distributed (its Schur operands live in per-rank temporaries)
-    if (!c.comm.on() && k > 0 && k < m && (m >= ns_min || (ns_env == 2 && m - k <= ns_pmax))) {
+    const bool nsbox = k > 0 && k < m && (m >= ns_min || (ns_env == 2 && m - k <= ns_pmax));
+    // §8(e): G_i arrives from owner(i); the R31 boxes are formed by every rank (their Schur
+    // operands C_p N and Y1 R_q are temporaries; by default their inverses are of size <= 64)
+    if (!nsbox && !c.mine(l, i, 2)) continue;
+    if (nsbox) {
       ns.push_back((int)a);
       continue;
     }
@@ -1727,7 +1729,7 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     int i = cs[a];
     const int m = f.m[i], k = f.k[i], n = m + k, pd = P.pdim[a];
     W[a] = c.work.d(std::max<size_t>((size_t)n * P.tot[a], 1));
-    if (!n || !c.mine(l, i, 2)) continue;
+    if (!n || (!pd && !c.mine(l, i, 2))) continue;
     if (pd) P.Rh[a] = c.work.d(std::max<size_t>((size_t)pd * P.tot[a], 1));
     for (auto& wq : P.wcol[a]) {
       const int q = wq.first;
@@ -1766,7 +1768,7 @@ static void eliminate_invert(Ctx& c, FLevel& f, const std::vector<int>& cs, Schu
     std::vector<std::vector<Region>> reg(c.comm.world);
     for (size_t a = 0; a < cs.size(); ++a) {
       const int i = cs[a], n = f.m[i] + f.k[i];
-      if (!n) continue;
+      if (!n || P.pdim[a]) continue;   // R31 boxes: formed by every rank
       auto& R = reg[c.own(l, i)];
       R.push_back(Region{f.rec[i].G, n, n, n});
       if (P.tot[a]) R.push_back(Region{W[a], n, n, P.tot[a]});
@@ -1797,6 +1799,23 @@ static void dbg_digest(Ctx& c, FLevel& f, const char* where) {
       }
   };
   for (int b : f.boxes) eat(0, f.U[b], f.m[b], f.m[b], f.k[b]);
+  static const bool per_box = getenv("AIFMM_DEBUG_DIST") && atoi(getenv("AIFMM_DEBUG_DIST")) == 2;
+  if (per_box && strstr(where, "compressed"))
+    for (int b : f.boxes) {
+      const int m = f.m[b], k = f.k[b];
+      std::vector<double> hb((size_t)m * std::max(k, 1));
+      if (k) AIFMM_CUDA(cudaMemcpyAsync(hb.data(), f.U[b], sizeof(double) * (size_t)m * k, cudaMemcpyDeviceToHost, c.s));
+      c.up.sync();
+      double n2 = 0, colsum = 0;
+      for (int j = 0; j < k; ++j) {
+        double cn = 0;
+        for (int i = 0; i < m; ++i) cn += hb[(size_t)j * m + i] * hb[(size_t)j * m + i];
+        n2 += cn;
+        colsum += std::fabs(cn - 1.0);
+      }
+      fprintf(stderr, "[dist %d] box L%d %s b=%d m=%d k=%d own=%d |U|^2=%.12e dev_from_unit=%.3e\n", c.comm.rank, f.l, where, b, m, k,
+              c.own(f.l, b), n2, colsum);
+    }
   BlkTable* T[3] = {&f.nearb, &f.A, &f.F};
   for (int w = 0; w < 3; ++w)
     for (size_t s = 0; s < T[w]->v.size(); ++s)

@@ -51,6 +51,7 @@ def _run_ranks(world, pts, b, kid, kp, leaf, tol, level_p=-1, algorithm=3):
             s = torch.cuda.Stream()
             with torch.cuda.stream(s), G.use(_lib(rank)):
                 G.free()
+                G.reset_counters()
                 G.set_algorithm(algorithm)
                 G.dist_init_local(rank, world, shared, level_p)
                 G.build(torch.from_numpy(pts).cuda(), kid, kp, leaf, tol)
@@ -180,3 +181,43 @@ print("nccl one-rank ok", int(st["dist_exchanges"]), rel)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "nccl one-rank ok" in r.stdout
+
+
+def test_distributed_config2_full_size():
+    """BASELINE config 2 at full size (N = 65536, 16 RHS, tol 1e-10) split over 2 and 4 in-process
+    ranks: replicas bitwise identical; against the single-GPU factorization the solution is
+    within the config-2 bar of tests/test_gpu_parity.py (max(10 tol, 1.5 x the oracle's own
+    rounding floor, reading R24): the split path differs from it only in rounding-level
+    decisions -- R31 off, other batch compositions) and the sampled direct-sum residual within
+    2x; the split FLOPs are balanced (largest rank <= 1.5 x an even share)."""
+    import json
+    import os
+    cfg = W.CONFIGS[1]
+    pts, b = W.make(cfg)
+    G.free()
+    G.build(torch.from_numpy(pts).cuda(), cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol)
+    G.factor()
+    Bd = torch.from_numpy(np.ascontiguousarray(b)).cuda()
+    X1 = G.solve(Bd)
+    x1 = X1.cpu().numpy()
+    rows = W.residual_rows(cfg.n, cfg.seed)
+    r1 = G.residual(X1, Bd, rows)
+    G.free()
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg2_oracle_rounding_floor.json")))
+    bar = max(10 * cfg.tol, 1.5 * g["same_decisions_rel_solution_diff"])
+    for world in (2, 4):
+        out = _run_ranks(world, pts, b, cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol)
+        x = out[0]["x"]
+        for r in range(1, world):
+            assert np.array_equal(out[r]["x"], x)
+        rel = np.linalg.norm(x - x1) / np.linalg.norm(x1)
+        G.free()
+        G.build(torch.from_numpy(pts).cuda(), cfg.kernel_id, cfg.kparams, cfg.leaf_size, cfg.tol)
+        rd = G.residual(torch.from_numpy(x).cuda(), Bd, rows)
+        G.free()
+        sch = [out[r]["stats"]["schur_flops"] for r in range(world)]
+        print(f"config 2 over {world} ranks: rel diff vs single GPU {rel:.2e} (bar {bar:.1e}), residual {rd:.3e} "
+              f"(single GPU {r1:.3e}), Schur FLOPs per rank {[round(v / 1e9, 1) for v in sch]} G")
+        assert rel <= bar, rel
+        assert rd <= 2 * r1, (rd, r1)
+        assert max(sch) <= 1.5 * sum(sch) / world
