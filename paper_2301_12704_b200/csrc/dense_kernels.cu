@@ -2208,6 +2208,33 @@ void launch_orth_sandwich(const void* v, const int* cnt, const int* idx, int nb,
 // ------------------------------------------------------------------------------ copies, norms
 __global__ void copy_tasks_kernel(const CopyTask* __restrict__ tasks) {
   const CopyTask tk = tasks[blockIdx.x];
+  if (tk.src && tk.trans) {
+    // transposed copy through a 32 x 32 shared-memory tile: src reads and dst writes both
+    // coalesced (same per-element arithmetic as below: alpha * src, then store / accumulate)
+    __shared__ double tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 8 rows of 32
+    const int tr = (tk.rows + 31) / 32, tcn = (tk.cols + 31) / 32;
+    for (int t = blockIdx.y; t < tr * tcn; t += gridDim.y) {
+      const int r0 = (t % tr) * 32, c0 = (t / tr) * 32;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {   // dst(r, c) = alpha * src[r * lds + c]: read along c
+        const int r = r0 + ty + 8 * i, c = c0 + tx;
+        if (r < tk.rows && c < tk.cols) tile[ty + 8 * i][tx] = tk.alpha * tk.src[(size_t)r * tk.lds + c];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {   // write along r
+        const int r = r0 + tx, c = c0 + ty + 8 * i;
+        if (r < tk.rows && c < tk.cols) {
+          double* d = tk.dst + (size_t)c * tk.ldd + r;
+          const double v = tile[tx][ty + 8 * i];
+          *d = tk.accumulate ? *d + v : v;
+        }
+      }
+      __syncthreads();
+    }
+    return;
+  }
   const int tot = tk.rows * tk.cols;
   for (int e = threadIdx.x + blockIdx.y * blockDim.x; e < tot; e += blockDim.x * gridDim.y) {
     const int r = e % tk.rows, c = e / tk.rows;
