@@ -30,6 +30,10 @@ constexpr int ACA_NT = 256;
 constexpr double ACA_TIE = 1e-10;
 constexpr double ACA_GUARD = 1e-13;
 constexpr int ACA_MAXR = 256;   // far ranges per box held in shared memory
+#ifndef ACA_JB_DEF
+#define ACA_JB_DEF 4
+#endif
+constexpr int ACA_JB = ACA_JB_DEF;   // residual-row columns per thread in flight
 
 template <int NT>
 __device__ __forceinline__ double bsum(double v, double* red) {
@@ -133,11 +137,27 @@ __global__ void __launch_bounds__(ACA_NT) aca_kernel(const AcaTask* __restrict__
     const int gi = tk.R[i];
     double* v = tk.Vw + (size_t)k * nF;
     double* u = tk.Uw + (size_t)k * nR;
-    // residual row r_j = A(R_i, F_j) - sum_t u_t[i] v_t[j]
-    for (int j = tid; j < nF; j += ACA_NT) {
-      double r = kernel_entry(kp, pts, gi, far_point(pre, st, nfr, j, tk.fidx));
-      for (int t = 0; t < k; ++t) r -= tk.Uw[(size_t)t * nR + i] * tk.Vw[(size_t)t * nF + j];
-      v[j] = r;
+    // residual row r_j = A(R_i, F_j) - sum_t u_t[i] v_t[j]; ACA_JB columns per thread in flight
+    // (independent chains: more loads of the cross history outstanding; each r_j still
+    // subtracts its terms in ascending t)
+    for (int j0 = tid; j0 < nF; j0 += ACA_NT * ACA_JB) {
+      double r[ACA_JB];
+#pragma unroll
+      for (int b = 0; b < ACA_JB; ++b) {
+        const int jj = j0 + b * ACA_NT;
+        r[b] = jj < nF ? kernel_entry(kp, pts, gi, far_point(pre, st, nfr, jj, tk.fidx)) : 0.0;
+      }
+      const double* Ui = tk.Uw + i;
+      for (int t = 0; t < k; ++t) {
+        const double ut = Ui[(size_t)t * nR];
+        const double* Vt = tk.Vw + (size_t)t * nF;
+#pragma unroll
+        for (int b = 0; b < ACA_JB; ++b)
+          if (j0 + b * ACA_NT < nF) r[b] -= ut * Vt[j0 + b * ACA_NT];
+      }
+#pragma unroll
+      for (int b = 0; b < ACA_JB; ++b)
+        if (j0 + b * ACA_NT < nF) v[j0 + b * ACA_NT] = r[b];
     }
     __syncthreads();
     const int j = pick_tw<ACA_NT>(v, tk.cused, nF, red, redi);
@@ -157,10 +177,20 @@ __global__ void __launch_bounds__(ACA_NT) aca_kernel(const AcaTask* __restrict__
     for (int q = tid; q < nF; q += ACA_NT) v[q] = v[q] / delta;
     const int gj = far_point(pre, st, nfr, j, tk.fidx);
     __syncthreads();
-    for (int q = tid; q < nR; q += ACA_NT) {
-      double c = kernel_entry(kp, pts, tk.R[q], gj);
-      for (int t = 0; t < k; ++t) c -= tk.Vw[(size_t)t * nF + j] * tk.Uw[(size_t)t * nR + q];
-      u[q] = c;
+    // residual column, two rows per thread in flight (each c_q in ascending t)
+    for (int q0 = tid; q0 < nR; q0 += 2 * ACA_NT) {
+      const int q1 = q0 + ACA_NT;
+      double c0 = kernel_entry(kp, pts, tk.R[q0], gj);
+      double c1 = q1 < nR ? kernel_entry(kp, pts, tk.R[q1], gj) : 0.0;
+      const double* Vj = tk.Vw + j;
+      for (int t = 0; t < k; ++t) {
+        const double vt = Vj[(size_t)t * nF];
+        const double* Ut = tk.Uw + (size_t)t * nR;
+        c0 -= vt * Ut[q0];
+        if (q1 < nR) c1 -= vt * Ut[q1];
+      }
+      u[q0] = c0;
+      if (q1 < nR) u[q1] = c1;
     }
     if (tid == 0) tk.cused[j] = 1;
     __syncthreads();
