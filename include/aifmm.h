@@ -219,7 +219,7 @@ int aifmm_set_timing(int on);
  * holding its median point -- contiguous Morton ranges of subtrees at the fine levels, one owner
  * per box at the coarse ones.
  * Owner computes, state replicated: every rank builds the same tree / lists / NNCA and holds
- * every block; in each colour of a level below l_p a rank compresses (RRQR) only
+ * every block; in each colour of a split level a rank compresses (RRQR) only
  * its own boxes, inverts only its own pivots and forms their multipliers, and
  * performs only the Schur updates (Table 4) of target blocks whose row box it owns;
  * each of these three phases ends with an exchange that gives every rank the blocks the others
@@ -244,7 +244,7 @@ int aifmm_set_timing(int on);
  *   first init, the same pointer for every rank) and exchange by device-to-device copies.
  * aifmm_dist_finalize — leave the communicator (back to the single-GPU path).
  * aifmm_get_owners — host int32[2^(d*level)]: owning rank of every box at `level` of the last
- *   factorization's partition (-1: computed redundantly, level <= l_p or not distributed).
+ *   factorization's partition (-1: computed redundantly, level <= level_p or not distributed).
  *   Errors: ESTATE before a build.
  * A rank that raises inside a distributed factorization leaves the others waiting in the next
  * exchange: errors are fatal for the job (as with any collective). */

@@ -1,19 +1,22 @@
 // dist.cuh — SURVEY §8(e): the subtree split of the factorisation across ranks (one process
 // per GPU), DESIGN.md §8.
 //
-// Model: owner computes, replicated state.  Every rank builds the same tree, lists, colours and
-// NNCA (cheap, deterministic) and holds every block of the factorisation.  The boxes of a
-// coarse level l_p are split into `world` contiguous Morton ranges of about equal point count;
-// a box at a finer level l > l_p belongs to the owner of its level-l_p ancestor.  Within each
-// colour phase of a level l > l_p the expensive batched work is split by ownership:
-//   * compression (RRQR stages 1 and 2) of a box b           -> owner(b)
-//   * pivot inverse G_i = P_i^-1 and multipliers W_i          -> owner(i)
-//   * Schur update of a target block (p, q)                   -> owner(p)
+// Model: owner computes, replicated state.  Every rank builds the same tree, lists and colours
+// and holds every block of the factorisation.  The points (tree order) are cut into `world`
+// contiguous ranges of equal size and a box belongs to the rank holding its median point
+// (contiguous Morton ranges of subtrees at the fine levels, one owner per box at the coarse
+// ones).  Within each colour phase of a split level the expensive batched work is split by
+// ownership:
+//   * NNCA pivot search (ACA) and skeleton solve of a box b     -> owner(b)   (build)
+//   * compression (RRQR stages 1 and 2) of a box b              -> owner(b)
+//   * pivot inverse G_i = P_i^-1 and multipliers W_i             -> owner(i)   (R31 boxes: all)
+//   * Schur update of a target block (p, q)                      -> owner(p)
 // and each phase ends with an exchange that hands every rank the blocks the others wrote (the
-// new basis columns and their ranks, G_i and W_i, the updated Schur targets).  Every block has
-// exactly one writer per phase and every reader runs after the exchange, so all ranks hold
-// bit-identical state after every phase; the cheap phases (level set-up, orthonormalisation,
-// redirection, new blocks, top level, solve) and the levels <= l_p run redundantly on every rank.
+// skeletons and operators, the new basis columns and their ranks, G_i and W_i, the updated Schur
+// targets).  Every block has exactly one writer per phase and every reader runs after the
+// exchange, so all ranks hold bit-identical state after every phase; the cheap phases (level
+// set-up, orthonormalisation, redirection, new blocks, top level, solve) and the levels
+// <= level_p (default: none) run redundantly on every rank.
 //
 // Two transports: NCCL (production: grouped in-place ncclBroadcast from each owner over
 // NVLink/NVSwitch, ncclAllReduce for the integer ranks), and an in-process transport for
