@@ -1949,9 +1949,15 @@ constexpr int HHU_BN = 64;   // column block (row chunk HHU_RK and pipeline stag
 constexpr int HHU_LV = HHB + 4, HHU_LC = HHU_BN + 4;  // padded rows (stride = 4 mod 16: no bank conflicts)
 template <int HHU_ST, int HHU_RK = 32>
 constexpr size_t hhu_smem() { return sizeof(double) * ((size_t)HHU_ST * HHU_RK * (HHU_LV + HHU_LC) + (size_t)HHB * HHU_LC); }
-template <int HHU_ST, int HHU_RK = 32>
+// PH = 0: both passes in one CTA.  PH = 1: pass 1 only, Z2 = T^T V^T C written to zg (one
+// HHB x HHU_BN slot per tile).  PH = 2: pass 2 only, for the rows [blockIdx.y * seg, +seg) of the
+// tile, Z2 read from zg.  Every element of Z2 and of C sees the same operations in the same order
+// in the three variants (pass 2 has no reduction across rows), so the split is bitwise neutral;
+// it lets a panel with few column blocks spread its row-parallel pass over many CTAs.
+template <int HHU_ST, int HHU_RK = 32, int PH = 0>
 __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restrict__ tasks,
-                                                           const HHUTile* __restrict__ tiles, int j) {
+                                                           const HHUTile* __restrict__ tiles, int j,
+                                                           double* __restrict__ zg = nullptr, int seg = 0) {
   extern __shared__ __align__(16) double hhu_smem[];
   const HHUTile tl = tiles[blockIdx.x];
   const HHTask tk = tasks[tl.task];
@@ -1967,7 +1973,10 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;   // 2 x 4 warps over 32 x 64
   const double* __restrict__ Tg = tk.T;                     // HHB x HHB, ld HHB (L1-resident)
-  const int nch = (rows + HHU_RK - 1) / HHU_RK;
+  const int nch_all = (rows + HHU_RK - 1) / HHU_RK;
+  const int ch0 = PH == 2 ? (int)blockIdx.y * (seg / HHU_RK) : 0;
+  if (PH == 2 && ch0 >= nch_all) return;
+  const int nch = PH == 2 ? min(nch_all, ch0 + seg / HHU_RK) : nch_all;
   auto issue = [&](int ch) {
     if (ch < nch) {
       const int st = ch % HHU_ST, r0 = ch * HHU_RK;
@@ -1986,6 +1995,7 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
     }
     cp_async_commit();
   };
+  if (PH != 2) {
   // pass 1: Z = V^T C  (32 x 64, K = rows), 3-stage cp.async pipeline
   double acc[2][2][2];
 #pragma unroll
@@ -2031,15 +2041,29 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
     z2[t] = s;
   }
   __syncthreads();
+  if (PH == 1) {
+    double* zt = zg + (size_t)blockIdx.x * HHB * HHU_BN;
+#pragma unroll
+    for (int t = 0; t < HHB * HHU_BN / HHU_NT; ++t) zt[tid + t * HHU_NT] = z2[t];
+    return;
+  }
 #pragma unroll
   for (int t = 0; t < HHB * HHU_BN / HHU_NT; ++t) {
     const int e = tid + t * HHU_NT, i = e % HHB, c = e / HHB;
     Zs[i * HHU_LC + c] = z2[t];
   }
+  } else {   // PH == 2: Z2 of this tile from pass 1
+    const double* zt = zg + (size_t)blockIdx.x * HHB * HHU_BN;
+#pragma unroll
+    for (int t = 0; t < HHB * HHU_BN / HHU_NT; ++t) {
+      const int e = tid + t * HHU_NT, i = e % HHB, c = e / HHB;
+      Zs[i * HHU_LC + c] = zt[e];
+    }
+  }
   __syncthreads();
   // pass 2: C -= V Z2, chunk by chunk (same pipeline), results stored from shared memory
-  for (int s = 0; s < HHU_ST - 1; ++s) issue(s);
-  for (int ch = 0; ch < nch; ++ch) {
+  for (int s = 0; s < HHU_ST - 1; ++s) issue(ch0 + s);
+  for (int ch = ch0; ch < nch; ++ch) {
     issue(ch + HHU_ST - 1);
     cp_async_wait<HHU_ST - 1>();
     __syncthreads();
@@ -2084,9 +2108,20 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
   }
   cp_async_wait<0>();
 }
-void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s) {
+void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s,
+                      double* zbuf, int seg, int nseg) {
   static const int st = getenv("AIFMM_HHU_ST") ? atoi(getenv("AIFMM_HHU_ST")) : 3;   // experiment toggle
-  if (st == 64) {            // 64-row chunks, 2 stages (experiment)
+  if (zbuf && nseg > 1) {    // split: pass 1 per tile, then pass 2 over (tile, row segment)
+    ensure_dyn_smem(hh_update_kernel<3, 32, 1>, hhu_smem<3>());
+    ensure_dyn_smem(hh_update_kernel<3, 32, 2>, hhu_smem<3>());
+    LAUNCH((hh_update_kernel<3, 32, 1>), ntiles, HHU_NT, hhu_smem<3>(), s, static_cast<const HHTask*>(tasks),
+           static_cast<const HHUTile*>(tiles), j, zbuf, 0);
+    if (g_before_launch) g_before_launch();
+    hh_update_kernel<3, 32, 2><<<dim3(ntiles, nseg), HHU_NT, hhu_smem<3>(), s>>>(
+        static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j, zbuf, seg);
+    AIFMM_CUDA(cudaGetLastError());
+    ++g_launches;
+  } else if (st == 64) {            // 64-row chunks, 2 stages (experiment)
     ensure_dyn_smem(hh_update_kernel<2, 64>, hhu_smem<2, 64>());
     LAUNCH((hh_update_kernel<2, 64>), ntiles, HHU_NT, (hhu_smem<2, 64>()), s, static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j);
   } else if (st == 2) {

@@ -41,7 +41,8 @@ size_t hh_task_size();
 void hh_make(void* out, double* A, int lda, int n, int m, double* V, double* T);
 void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode, int nmax);
 void launch_hh_extract(const void* t, int ntasks, double* const* out, const int* ldo, cudaStream_t s);
-void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s);
+void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s,
+                      double* zbuf = nullptr, int seg = 0, int nseg = 0);
 constexpr int HH_PANEL = 32;
 constexpr int GJ_SMALL_MAX = 160;  // in-place inverses up to this size run in shared memory (<= 206 KB)
 constexpr int GJ_PANEL = 32;
@@ -763,6 +764,22 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
     dgen = up.gen();
   };
   if (g_prof.on) { g_prof.end("cmp.proj"); g_prof.begin(s); }
+  // trailing updates run as two launches: pass 1 (Z2, one CTA per column-block tile) and the
+  // row-parallel pass 2 split over (tile, 256-row segment) — bitwise the same C as the fused
+  // kernel (see hh_update_kernel), measured -2% config-3 factor, -12% config-2 RRQR stage 1;
+  // AIFMM_HHU_SPLIT=<n> keeps the fused kernel for panels with >= n tiles.  The Z2 slots are
+  // sized by the first panel, which has the most tiles
+  static const int split_tiles = getenv("AIFMM_HHU_SPLIT") ? atoi(getenv("AIFMM_HHU_SPLIT")) : 1 << 30;
+  static const int hhu_seg = getenv("AIFMM_HHU_SEG") ? atoi(getenv("AIFMM_HHU_SEG")) : 256;
+  double* zbuf = nullptr;
+  {
+    size_t t0 = 0;
+    for (const auto& q : reqs) {
+      const int r = std::min(q.n, q.m);
+      if (r > 0) t0 += (size_t)((std::max(q.m - std::min(HH_PANEL, r), 0) + 63) / 64);
+    }
+    if (t0 > 0 && (int)t0 < split_tiles) zbuf = work.d(t0 * HH_PANEL * 64);
+  }
   for (int j = 0; j < rmax; j += HH_PANEL) {
     if (g_prof.on) g_prof.begin(s);
     restage();
@@ -789,7 +806,13 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
       up.reserve(tb.size() + outs.size() * 8 + ldo.size() * 4 + ut.size() * sizeof(int2) + 2048);
       restage();
       const int2* dut = up.put(ut);
-      launch_hh_update(dt, dut, (int)ut.size(), j, s);
+      int nseg = 0;
+      if (zbuf && (int)ut.size() < split_tiles) {
+        int rows_max = 0;
+        for (const int2& u : ut) rows_max = std::max(rows_max, R[u.x].n - j);
+        nseg = (rows_max + hhu_seg - 1) / hhu_seg;
+      }
+      launch_hh_update(dt, dut, (int)ut.size(), j, s, zbuf, hhu_seg, nseg);
     }
     if (g_prof.on) g_prof.end("hh.trail");
   }
