@@ -1947,8 +1947,11 @@ struct HHUTile { int task, n0; };
 constexpr int HHU_NT = 256;
 constexpr int HHU_BN = 64;   // column block (row chunk HHU_RK and pipeline stages: template)
 constexpr int HHU_LV = HHB + 4, HHU_LC = HHU_BN + 4;  // padded rows (stride = 4 mod 16: no bank conflicts)
-template <int HHU_ST, int HHU_RK = 32>
-constexpr size_t hhu_smem() { return sizeof(double) * ((size_t)HHU_ST * HHU_RK * (HHU_LV + HHU_LC) + (size_t)HHB * HHU_LC); }
+// (pass 1 alone keeps Z in the stage buffers, which are idle once its K loop has drained)
+template <int HHU_ST, int HHU_RK = 32, int PH = 0>
+constexpr size_t hhu_smem() {
+  return sizeof(double) * ((size_t)HHU_ST * HHU_RK * (HHU_LV + HHU_LC) + (PH == 1 ? 0 : (size_t)HHB * HHU_LC));
+}
 // PH = 0: both passes in one CTA.  PH = 1: pass 1 only, Z2 = T^T V^T C written to zg (one
 // HHB x HHU_BN slot per tile).  PH = 2: pass 2 only, for the rows [blockIdx.y * seg, +seg) of the
 // tile, Z2 read from zg.  Every element of Z2 and of C sees the same operations in the same order
@@ -1969,7 +1972,7 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
   const double* V = tk.V;
   double* Vs = hhu_smem;                                  // [ST][RK][LV]
   double* Cs = Vs + (size_t)HHU_ST * HHU_RK * HHU_LV;     // [ST][RK][LC]
-  double* Zs = Cs + (size_t)HHU_ST * HHU_RK * HHU_LC;     // [HHB][LC]
+  double* Zs = PH == 1 ? hhu_smem : Cs + (size_t)HHU_ST * HHU_RK * HHU_LC;   // [HHB][LC]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;   // 2 x 4 warps over 32 x 64
   const double* __restrict__ Tg = tk.T;                     // HHB x HHB, ld HHB (L1-resident)
@@ -2112,13 +2115,29 @@ void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, c
                       double* zbuf, int seg, int nseg) {
   static const int st = getenv("AIFMM_HHU_ST") ? atoi(getenv("AIFMM_HHU_ST")) : 3;   // experiment toggle
   if (zbuf && nseg > 1) {    // split: pass 1 per tile, then pass 2 over (tile, row segment)
-    ensure_dyn_smem(hh_update_kernel<3, 32, 1>, hhu_smem<3>());
-    ensure_dyn_smem(hh_update_kernel<3, 32, 2>, hhu_smem<3>());
-    LAUNCH((hh_update_kernel<3, 32, 1>), ntiles, HHU_NT, hhu_smem<3>(), s, static_cast<const HHTask*>(tasks),
-           static_cast<const HHUTile*>(tiles), j, zbuf, 0);
+    // pipeline variants (same arithmetic order; shared memory sets the CTAs per SM)
+    static const int p1 = getenv("AIFMM_HHU_P1") ? atoi(getenv("AIFMM_HHU_P1")) : 3;
+    static const int p2 = getenv("AIFMM_HHU_P2") ? atoi(getenv("AIFMM_HHU_P2")) : 3;
+    const HHTask* tk = static_cast<const HHTask*>(tasks);
+    const HHUTile* tt = static_cast<const HHUTile*>(tiles);
+    if (p1 == 2) {
+      ensure_dyn_smem(hh_update_kernel<2, 32, 1>, hhu_smem<2, 32, 1>());
+      LAUNCH((hh_update_kernel<2, 32, 1>), ntiles, HHU_NT, (hhu_smem<2, 32, 1>()), s, tk, tt, j, zbuf, 0);
+    } else if (p1 == 4) {
+      ensure_dyn_smem(hh_update_kernel<4, 16, 1>, hhu_smem<4, 16, 1>());
+      LAUNCH((hh_update_kernel<4, 16, 1>), ntiles, HHU_NT, (hhu_smem<4, 16, 1>()), s, tk, tt, j, zbuf, 0);
+    } else {
+      ensure_dyn_smem(hh_update_kernel<3, 32, 1>, hhu_smem<3, 32, 1>());
+      LAUNCH((hh_update_kernel<3, 32, 1>), ntiles, HHU_NT, (hhu_smem<3, 32, 1>()), s, tk, tt, j, zbuf, 0);
+    }
     if (g_before_launch) g_before_launch();
-    hh_update_kernel<3, 32, 2><<<dim3(ntiles, nseg), HHU_NT, hhu_smem<3>(), s>>>(
-        static_cast<const HHTask*>(tasks), static_cast<const HHUTile*>(tiles), j, zbuf, seg);
+    if (p2 == 2) {
+      ensure_dyn_smem(hh_update_kernel<2, 32, 2>, hhu_smem<2, 32, 2>());
+      hh_update_kernel<2, 32, 2><<<dim3(ntiles, nseg), HHU_NT, hhu_smem<2, 32, 2>(), s>>>(tk, tt, j, zbuf, seg);
+    } else {
+      ensure_dyn_smem(hh_update_kernel<3, 32, 2>, hhu_smem<3, 32, 2>());
+      hh_update_kernel<3, 32, 2><<<dim3(ntiles, nseg), HHU_NT, hhu_smem<3, 32, 2>(), s>>>(tk, tt, j, zbuf, seg);
+    }
     AIFMM_CUDA(cudaGetLastError());
     ++g_launches;
   } else if (st == 64) {            // 64-row chunks, 2 stages (experiment)
