@@ -2111,6 +2111,24 @@ __global__ void __launch_bounds__(HHU_NT) hh_update_kernel(const HHTask* __restr
   }
   cp_async_wait<0>();
 }
+// one pass of the split trailing update (look-ahead schedule: pass 2 of the next panel's
+// column tile runs first, the other tiles' pass 2 on a second stream under the next panel)
+void launch_hh_update_pass(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s,
+                           double* zbuf, int seg, int nseg, int pass) {
+  if (ntiles <= 0) return;
+  const HHTask* tk = static_cast<const HHTask*>(tasks);
+  const HHUTile* tt = static_cast<const HHUTile*>(tiles);
+  if (pass == 1) {
+    ensure_dyn_smem(hh_update_kernel<3, 32, 1>, hhu_smem<3, 32, 1>());
+    LAUNCH((hh_update_kernel<3, 32, 1>), ntiles, HHU_NT, (hhu_smem<3, 32, 1>()), s, tk, tt, j, zbuf, 0);
+  } else {
+    ensure_dyn_smem(hh_update_kernel<3, 32, 2>, hhu_smem<3, 32, 2>());
+    if (g_before_launch) g_before_launch();
+    hh_update_kernel<3, 32, 2><<<dim3(ntiles, nseg), HHU_NT, hhu_smem<3, 32, 2>(), s>>>(tk, tt, j, zbuf, seg);
+    AIFMM_CUDA(cudaGetLastError());
+    ++g_launches;
+  }
+}
 void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s,
                       double* zbuf, int seg, int nseg) {
   static const int st = getenv("AIFMM_HHU_ST") ? atoi(getenv("AIFMM_HHU_ST")) : 3;   // experiment toggle

@@ -43,6 +43,8 @@ void launch_hh_panel(const void* t, int ntasks, int j, cudaStream_t s, int mode,
 void launch_hh_extract(const void* t, int ntasks, double* const* out, const int* ldo, cudaStream_t s);
 void launch_hh_update(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s,
                       double* zbuf = nullptr, int seg = 0, int nseg = 0);
+void launch_hh_update_pass(const void* tasks, const void* tiles, int ntiles, int j, cudaStream_t s,
+                           double* zbuf, int seg, int nseg, int pass);
 constexpr int HH_PANEL = 32;
 constexpr int GJ_SMALL_MAX = 160;  // in-place inverses up to this size run in shared memory (<= 206 KB)
 constexpr int GJ_PANEL = 32;
@@ -736,6 +738,10 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
   for (const auto& q : reqs) if (q.n > SM_LIM && !many && q.n > SM_ROWS) sorted_reqs.push_back(q);
   const std::vector<TriRootReq>& R = sorted_reqs;
   std::vector<char> tb(tsz * reqs.size());
+  // look-ahead schedule (opt-in): the descriptors of odd panels point at a second V / T pair,
+  // so panel p + 1 can run while the other column tiles of panel p's update still read V / T
+  static const bool lookahead = getenv("AIFMM_HHU_LOOKAHEAD") != nullptr;
+  std::vector<char> tb2(lookahead ? tsz * reqs.size() : 0);
   std::vector<double*> V(reqs.size()), T(reqs.size());
   std::vector<double*> outs(reqs.size());
   std::vector<int> ldo(reqs.size());
@@ -745,20 +751,25 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
     V[i] = work.d((size_t)std::max(q.n, 1) * HH_PANEL);
     T[i] = work.d((size_t)HH_PANEL * HH_PANEL);
     hh_make(tb.data() + i * tsz, q.A, q.lda, q.n, q.m, V[i], T[i]);
+    if (lookahead)
+      hh_make(tb2.data() + i * tsz, q.A, q.lda, q.n, q.m, work.d((size_t)std::max(q.n, 1) * HH_PANEL),
+              work.d((size_t)HH_PANEL * HH_PANEL));
     outs[i] = q.out;
     ldo[i] = q.ldm;
     rmax = std::max(rmax, std::min(q.n, q.m));
     if (fc) fc->flops += 2.0 * q.n * (double)q.m * q.m;
   }
-  up.reserve(tb.size() + outs.size() * 8 + ldo.size() * 4 + 1024);
+  up.reserve(2 * tb.size() + outs.size() * 8 + ldo.size() * 4 + 1024);
   const void* dt = up.put(tb.data(), tb.size());
+  const void* dt2 = lookahead ? up.put(tb2.data(), tb2.size()) : nullptr;
   double* const* douts = up.put(outs);
   const int* dldo = up.put(ldo);
   unsigned long long dgen = up.gen();
   auto restage = [&] {   // the staging arena was rewound by a sync: upload the descriptors again
     if (up.gen() == dgen) return;
-    up.reserve(tb.size() + outs.size() * 8 + ldo.size() * 4 + 1024);
+    up.reserve(2 * tb.size() + outs.size() * 8 + ldo.size() * 4 + 1024);
     dt = up.put(tb.data(), tb.size());
+    if (lookahead) dt2 = up.put(tb2.data(), tb2.size());
     douts = up.put(outs);
     dldo = up.put(ldo);
     dgen = up.gen();
@@ -780,10 +791,20 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
     }
     if (t0 > 0 && (int)t0 < split_tiles) zbuf = work.d(t0 * HH_PANEL * 64);
   }
+  const bool la = lookahead && zbuf && !g_prof.on;
+  static cudaStream_t s2 = nullptr;
+  static cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  if (la && !s2) {
+    AIFMM_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    AIFMM_CUDA(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
+    AIFMM_CUDA(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
+  }
+  bool rest_pending = false;   // ev_b marks the side stream's last pass 2
   for (int j = 0; j < rmax; j += HH_PANEL) {
     if (g_prof.on) g_prof.begin(s);
     restage();
-    const char* d0 = static_cast<const char*>(dt);
+    const void* dcur = (la && ((j / HH_PANEL) & 1)) ? dt2 : dt;
+    const char* d0 = static_cast<const char*>(dcur);
     const size_t o1 = nrg, o2 = o1 + nsm, o3 = o2 + nsmall, o4 = o3 + nrc, o5 = o4 + nmid;
     if (nrg && j < nmax_rg) launch_hh_panel(d0, (int)nrg, j, s, 4, nmax_rg);
     if (nsm && j < nmax_sm) launch_hh_panel(d0 + o1 * tsz, (int)nsm, j, s, use_smem ? 3 : 6, nmax_sm);
@@ -799,7 +820,21 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
       if (j >= r) continue;
       const int nbw = std::min(HH_PANEL, r - j);
       const int nc = q.m - j - nbw;
-      for (int n0 = 0; n0 < nc; n0 += 64) ut.push_back(make_int2((int)i, n0));
+      for (int n0 = 0; n0 < nc; n0 += 64)
+        if (!la || n0 == 0) ut.push_back(make_int2((int)i, n0));
+    }
+    const size_t n_first = ut.size();   // look-ahead: the tiles holding the next panel come first
+    if (la)
+      for (size_t i = 0; i < reqs.size(); ++i) {
+        const TriRootReq& q = R[i];
+        const int r = std::min(q.n, q.m);
+        if (j >= r) continue;
+        const int nc = q.m - j - std::min(HH_PANEL, r - j);
+        for (int n0 = 64; n0 < nc; n0 += 64) ut.push_back(make_int2((int)i, n0));
+      }
+    if (la && rest_pending) {   // pass 1 reads the columns the side stream was still updating
+      AIFMM_CUDA(cudaStreamWaitEvent(s, ev_b, 0));
+      rest_pending = false;
     }
     if (g_prof.on) { g_prof.end("hh.panel"); g_prof.begin(s); }
     if (!ut.empty()) {
@@ -812,10 +847,24 @@ inline void batched_tri_root(const std::vector<TriRootReq>& reqs_in, Pool& work,
         for (const int2& u : ut) rows_max = std::max(rows_max, R[u.x].n - j);
         nseg = (rows_max + hhu_seg - 1) / hhu_seg;
       }
-      launch_hh_update(dt, dut, (int)ut.size(), j, s, zbuf, hhu_seg, nseg);
+      if (la) {
+        launch_hh_update_pass(dcur, dut, (int)ut.size(), j, s, zbuf, hhu_seg, nseg, 1);
+        launch_hh_update_pass(dcur, dut, (int)n_first, j, s, zbuf, hhu_seg, nseg, 2);
+        if (ut.size() > n_first) {
+          AIFMM_CUDA(cudaEventRecord(ev_a, s));
+          AIFMM_CUDA(cudaStreamWaitEvent(s2, ev_a, 0));
+          launch_hh_update_pass(dcur, dut + n_first, (int)(ut.size() - n_first), j, s2,
+                                zbuf + n_first * HH_PANEL * 64, hhu_seg, nseg, 2);
+          AIFMM_CUDA(cudaEventRecord(ev_b, s2));
+          rest_pending = true;
+        }
+      } else {
+        launch_hh_update(dcur, dut, (int)ut.size(), j, s, zbuf, hhu_seg, nseg);
+      }
     }
     if (g_prof.on) g_prof.end("hh.trail");
   }
+  if (rest_pending) AIFMM_CUDA(cudaStreamWaitEvent(s, ev_b, 0));
   if (g_prof.on) g_prof.begin(s);
   restage();
   launch_hh_extract(dt, (int)reqs.size(), douts, dldo, s);
